@@ -1,0 +1,76 @@
+"""Oracle misfit / gradient pins: Taylor test (§6.1), zero residual at the true
+model, source-sum linearity, and the E^T reading R11."""
+import numpy as np
+
+import synth
+from oracle import discretize as D
+from oracle import fwi
+
+
+def _setup():
+    p = synth.tiny2d()
+    pml = D.PmlParams(v_ref=3000.0)          # fixed: H depends on m only via Eq. (7)
+    d = fwi.forward_data(p, pml, p.m_true)
+    return p, pml, d
+
+
+def _slopes(e, ts):
+    return np.log2(e[:-1] / e[1:])
+
+
+def test_taylor_first_and_second_order():
+    p, pml, d = _setup()
+    f0, g = fwi.misfit_grad(p, pml, d)
+    dm = p.m_true - p.m                      # physically meaningful direction
+    ts = 2.0 ** -np.arange(2, 10)
+    e0, e1 = fwi.taylor_errors(lambda m: fwi.misfit_grad(p, pml, d, m)[0], p.m, dm, g, ts)
+    s0, s1 = _slopes(e0, ts), _slopes(e1, ts)
+    assert np.all(np.abs(s0 - 1) < 0.25), s0         # O(h)   (P:318 line 1)
+    assert np.all(np.abs(s1 - 2) < 0.25), s1         # O(h^2) (P:318 line 2)
+
+
+def test_interior_only_gradient_fails_taylor():
+    """R11: restricting Re(w^2 conj(u) v) to the interior (instead of E^T) loses second order."""
+    p, pml, d = _setup()
+    _, g = fwi.misfit_grad(p, pml, d)
+    # rebuild g without the E^T fold: interior samples of g_ext only
+    w = 2 * np.pi * p.freqs[0]
+    f, g_full, fields = fwi.misfit_grad(p, pml, d, return_fields=True)
+    U, V = fields[0]
+    gext = np.sum(np.real(w**2 * np.conj(U) * V), axis=1).reshape(D.ext_shape(p))
+    (xl, _), _, (zl, _) = p.pml
+    g_int = gext[zl:zl + p.n[2], :, xl:xl + p.n[0]]
+    assert np.linalg.norm(g_int - g_full) / np.linalg.norm(g_full) > 1e-3
+    dm = synth.random_real(p.m.shape, 2) * np.abs(p.m).max() * 0.05   # touches boundary cells
+    ts = 2.0 ** -np.arange(4, 12)
+    _, e1 = fwi.taylor_errors(lambda m: fwi.misfit_grad(p, pml, d, m)[0], p.m, dm, g_int, ts)
+    assert np.median(_slopes(e1, ts)) < 1.5
+
+
+def test_zero_residual_at_true_model():
+    p, pml, d = _setup()
+    f, g = fwi.misfit_grad(p, pml, d, p.m_true)
+    f0, _ = fwi.misfit_grad(p, pml, d)
+    assert f <= 1e-20 * max(f0, 1.0) + 1e-24
+    assert np.abs(g).max() < 1e-10 * np.abs(fwi.misfit_grad(p, pml, d)[1]).max()
+
+
+def test_source_sum_linearity():
+    p, pml, d = _setup()
+    fa, ga = fwi.misfit_grad(p, pml, d[:, :1], src_ids=p.src[:1])
+    fb, gb = fwi.misfit_grad(p, pml, d[:, 1:], src_ids=p.src[1:])
+    f, g = fwi.misfit_grad(p, pml, d)
+    assert abs(fa + fb - f) <= 1e-12 * f
+    assert np.linalg.norm(ga + gb - g) <= 1e-12 * np.linalg.norm(g)
+
+
+def test_gradient_matches_directional_difference():
+    """Central difference of f along a smooth direction agrees with <g, dm> to O(t^2)."""
+    p, pml, d = _setup()
+    _, g = fwi.misfit_grad(p, pml, d)
+    dm = np.ones_like(p.m) * 1e-9
+    t = 1e-2
+    fp = fwi.misfit_grad(p, pml, d, p.m + t * dm)[0]
+    fm = fwi.misfit_grad(p, pml, d, p.m - t * dm)[0]
+    fd = (fp - fm) / (2 * t)
+    assert abs(fd - np.sum(g * dm)) <= 1e-6 * abs(fd)
