@@ -1,0 +1,163 @@
+/*
+ * helm.h — C ABI of libhelm.so, the B200 (sm_100a) hot path of arXiv 1703.09268:
+ * the per-source, per-frequency PML Helmholtz solve (FGMRES + ML-GMRES) feeding the
+ * least-squares misfit and its adjoint-state gradient.
+ *
+ * Citations: P:n = line n of the paper text,
+ *            D<k>/R<k> = SURVEY.md §8(c) definitions / readings (restated in DESIGN.md).
+ *
+ * Conventions (every entry point):
+ *  - Layout. Complex arrays are interleaved (re, im), C-order [rhs][z][y][x], x fastest,
+ *    on the PML-EXTENDED grid (N_a = n_a + pml[a][0] + pml[a][1]). 2D problems are (x, z):
+ *    ndim = 2, n[1] = 1, pml[1] = {0, 0}. Models are real, INTERIOR, x fastest.
+ *  - Ownership. The caller owns every pointer argument. Host arrays are copied before the
+ *    call returns. Device arrays are caller-allocated (cudaMalloc / torch) and must be
+ *    8-byte aligned (16 for complex128). A helm_op owns its device copies of the model,
+ *    the 1D PML tables, the level hierarchy, the Krylov workspace for max_rhs right-hand
+ *    sides and its captured CUDA graphs; helm_destroy frees them.
+ *  - Streams. Work is ordered on `cuda_stream` (cudaStream_t, NULL = legacy default).
+ *    helm_apply is asynchronous. helm_setup, helm_solve, fwi_* return after completion.
+ *  - Concurrency. One helm_op must not be used from two threads/streams at once.
+ *  - Errors. A negative status means nothing was written to the outputs (argument and
+ *    shape checks run before any work). CUDA / allocation failures return
+ *    HELM_ERR_CUDA / HELM_ERR_OOM. helm_last_error() gives thread-local text for the last
+ *    non-OK status (and for warnings, e.g. < 4 points per wavelength, with HELM_OK).
+ *  - There is no CPU fallback: every numeric step runs in this library's CUDA kernels.
+ */
+#ifndef HELM_H
+#define HELM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HELM_OK = 0,
+  HELM_ERR_ARG = -1,    /* bad scalar argument / NULL pointer */
+  HELM_ERR_SHAPE = -2,  /* sizes inconsistent (nrhs > max_rhs, grid too small, ...) */
+  HELM_ERR_CUDA = -3,   /* CUDA runtime error (text in helm_last_error) */
+  HELM_ERR_OOM = -4,    /* device allocation failed */
+  HELM_ERR_STATE = -5   /* library / device not usable (no sm_100 device, ...) */
+} helm_status;
+
+/* D15 / R26. HELM_C128: everything complex128, fp64 reductions.
+ * HELM_C64 ("mixed"): user-visible complex arrays are complex64; the stencil, the V-cycle
+ * and the smoother / coarse Krylov bases run in complex64 with fp32 tables and model; the
+ * outer FGMRES (its basis, iterate, true residual and matvec) runs in complex128 against
+ * the fp64 operator, so solves reach the fp64 operator's rel-residual target. */
+typedef enum { HELM_C64 = 0, HELM_C128 = 1 } helm_dtype;
+
+/* D1. Interior grid; PML points per axis and side. */
+typedef struct {
+  int32_t ndim;        /* 2 (x,z) or 3 (x,y,z) */
+  int64_t n[3];        /* interior points per axis, x first (n[1] = 1 in 2D) */
+  double h;            /* uniform spacing [m], > 0 */
+  int32_t pml[3][2];   /* PML points per axis per side (pml[1] = {0,0} in 2D) */
+} helm_grid;
+
+/* D3 / R5. sigma(d) = sigma_max (d/L)^power, sigma_max = (power+1) v_ref ln(1/R) / (2L),
+ * eta = 1 + i sigma/omega (R3). v_ref <= 0 in helm_setup means "max velocity of m";
+ * fwi_* require v_ref > 0 so that H depends on m only through omega^2 diag(E m) (Eq. 7). */
+typedef struct { double R; int32_t power; double v_ref; } helm_pml;
+
+/* §5: memory vector (k_so, k_si, k_co, k_ci) = (3,5,3,5), levels = 3 grids (R20). */
+typedef struct { int32_t levels, ks_o, ks_i, kc_o, kc_i; } helm_mlopts;
+
+/* outer FGMRES(k_inner) restarted until the TRUE ||b - Hx||/||b|| <= rtol per RHS
+ * (R23), x0 = 0; precond 1 = ML-GMRES, 0 = none (plain restarted GMRES(k_inner)). */
+typedef struct { int32_t k_inner, max_outer; double rtol; int32_t precond; } helm_solve_opts;
+
+/* Per right-hand side. matvecs[l] = operator applications on level l (fine = 0);
+ * bytes_alg = algorithmic HBM bytes the kernels of this solve moved for this RHS
+ * (DESIGN.md §6 per-kernel formulas). Non-convergence is NOT an error: converged = 0. */
+typedef struct {
+  int32_t outer_cycles, converged;
+  double rel_residual;
+  int64_t matvecs[4];
+  double bytes_alg;
+} helm_solve_report;
+
+typedef struct helm_op helm_op;   /* opaque */
+
+/* a1 (Fig. 3). Builds, on the device: m_ext = E m (D2), the per
+ * level / per axis complex 1D tables (lo, dg, up) of H and of H^H (D4, D6), the coarse
+ * models by normalized full weighting and their tables (D13), and the Krylov workspace for
+ * `max_rhs` right-hand sides. omega = 2 pi f [rad/s] > 0. mlopts NULL = defaults.
+ * m_slowness2: host, interior, n[0]*n[1]*n[2] doubles, x fastest (R1: m = 1/v^2). */
+helm_status helm_setup(const helm_grid* grid, const double* m_slowness2, double omega,
+                       const helm_pml* pml, helm_dtype dtype, int32_t max_rhs,
+                       const helm_mlopts* mlopts, void* cuda_stream, helm_op** out);
+
+/* a2 (Eq. 1). y = H x (adjoint = 0) or y = H^H x (adjoint = 1) for
+ * nrhs right-hand sides on the finest extended grid; x, y device, dtype of the op, must not
+ * alias. H = sum_a T_a + omega^2 diag(E m) (D5), zero Dirichlet ghosts (R7). */
+helm_status helm_apply(helm_op* op, int32_t adjoint, int32_t nrhs, const void* x_dev,
+                       void* y_dev, void* cuda_stream);
+
+/* a3-a6 (+a8 with adjoint = 1). Solves H x = b (or H^H x = b) for nrhs independent RHS
+ * (R27) with FGMRES(k_inner) + ML-GMRES. b_dev, x_dev: device, extended grid, dtype of the
+ * op; x_dev is output only (x0 = 0). report_host: NULL or an array of nrhs reports. */
+helm_status helm_solve(helm_op* op, int32_t adjoint, int32_t nrhs, const void* b_dev,
+                       void* x_dev, const helm_solve_opts* opts,
+                       helm_solve_report* report_host, void* cuda_stream);
+
+/* a1-a9 (Listing 1 `case OBJ`; Eq. 2; Eq. 8; D7-D12). For each
+ * frequency and each source s in [src_begin, src_end):
+ *   u = H^-1 q_s, q_s = S e_node(s)/h^d;  f += 1/2 ||P_r u - d||^2;
+ *   v = H^-H(-P_r^T(P_r u - d));        g += E^T Re(omega^2 conj(u) v).
+ * Sources are solved in batches of at most `max_rhs`. src_node / rec_node: host, interior
+ * linear node ids (ix + nx*(iy + ny*iz)); receivers must be distinct. d_obs_reim: host
+ * complex128 [nfreq][nsrc_total][nrec]. src_weight_reim: host complex128 [nfreq] or NULL
+ * (S = 1). fg_dev: device fp64 [1 + n_interior], overwritten with f then g (interior, x
+ * fastest); the multi-GPU sum is the caller's all_reduce over this buffer.
+ * report_host: NULL or [nfreq][src_end - src_begin][2] (forward, adjoint). */
+helm_status fwi_misfit_grad(const helm_grid* grid, const double* m_slowness2, int32_t nfreq,
+                            const double* freq_hz, const double* src_weight_reim,
+                            int32_t nsrc_total, int32_t src_begin, int32_t src_end,
+                            const int64_t* src_node, int32_t nrec, const int64_t* rec_node,
+                            const double* d_obs_reim, const helm_pml* pml, helm_dtype dtype,
+                            const helm_solve_opts* opts, int32_t max_rhs, double* fg_dev,
+                            helm_solve_report* report_host, void* cuda_stream);
+
+/* Listing 1 `case FORW_MODEL`: d[f][s][k] = (P_r H_f^-1 q_s)_k for s in
+ * [src_begin, src_end). d_host: host complex128 [nfreq][src_end - src_begin][nrec]. */
+helm_status fwi_forward(const helm_grid* grid, const double* m_slowness2, int32_t nfreq,
+                        const double* freq_hz, const double* src_weight_reim,
+                        int32_t src_begin, int32_t src_end, const int64_t* src_node,
+                        int32_t nrec, const int64_t* rec_node, const helm_pml* pml,
+                        helm_dtype dtype, const helm_solve_opts* opts, int32_t max_rhs,
+                        double* d_host, helm_solve_report* report_host, void* cuda_stream);
+
+/* ---- inspection entry points (same op; used by the parity tests) ---------------------- */
+
+/* Number of levels and per-level extended sizes (x, y, z). dims_host: [levels][3]. */
+helm_status helm_levels(const helm_op* op, int32_t* levels, int64_t* dims_host);
+
+/* Copies level `level`'s 1D tables (complex128, [3 axes][3 = lo,dg,up][Nmax]) for H
+ * (adjoint 0) or H^H (adjoint 1), and its model (fp64, extended, x fastest). */
+helm_status helm_get_level(const helm_op* op, int32_t level, int32_t adjoint, int64_t nmax,
+                           double* tables_host, double* m_host);
+
+/* One ML-GMRES V-cycle z = M_l(b) at level `level` (Alg. 1 + Fig. 3 recursion, fixed
+ * counts D14), b and z device arrays of the op's dtype on that level's grid. */
+helm_status helm_vcycle(helm_op* op, int32_t level, int32_t adjoint, int32_t nrhs,
+                        const void* b_dev, void* z_dev, void* cuda_stream);
+
+/* Level transfer (D13): restrict (R = 2^-d P^T, fine level -> level+1) or prolong-add
+ * (x_fine += P x_coarse), dtype of the op. */
+helm_status helm_transfer(helm_op* op, int32_t level, int32_t prolong, int32_t nrhs,
+                          const void* in_dev, void* out_dev, void* cuda_stream);
+
+/* Peak live workspace of a solve, in vectors of the finest size per RHS. */
+double      helm_workspace_vectors(const helm_op* op);
+
+void        helm_destroy(helm_op* op);
+const char* helm_last_error(void);
+const char* helm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HELM_H */

@@ -1,0 +1,243 @@
+"""Thin Python binding of include/helm.h with the same entry-point names.
+
+Argument marshalling only: every numeric step runs in libhelm.so's CUDA kernels. torch
+supplies device memory and the current CUDA stream (plumbing, not the product).
+Complex device arrays are torch tensors of dtype complex64 / complex128 on the extended
+grid, shape (nrhs, Nz, Ny, Nx) (or anything contiguous with that many elements).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+C64, C128 = L.HELM_C64, L.HELM_C128
+TORCH_DTYPE = {C64: torch.complex64, C128: torch.complex128}
+
+
+@dataclasses.dataclass(frozen=True)
+class Grid:
+    """D1: interior sizes (nx, ny, nz) (ny = 1 in 2D), spacing h, PML ((xl,xh),(yl,yh),(zl,zh))."""
+    ndim: int
+    n: Tuple[int, int, int]
+    h: float
+    pml: Tuple[Tuple[int, int], ...]
+
+    @staticmethod
+    def of(p) -> "Grid":
+        return Grid(int(p.ndim), tuple(int(v) for v in p.n), float(p.h), tuple(tuple(int(w) for w in a) for a in p.pml))
+
+    @property
+    def next(self):
+        return tuple(self.n[a] + self.pml[a][0] + self.pml[a][1] for a in range(3))
+
+    @property
+    def n_ext(self):
+        return int(np.prod(self.next))
+
+    @property
+    def n_interior(self):
+        return int(np.prod(self.n))
+
+    def c(self) -> L.HelmGrid:
+        g = L.HelmGrid()
+        g.ndim = self.ndim
+        for a in range(3):
+            g.n[a] = self.n[a]
+            g.pml[a][0], g.pml[a][1] = self.pml[a]
+        g.h = self.h
+        return g
+
+
+@dataclasses.dataclass(frozen=True)
+class Pml:
+    R: float = 1e-4
+    power: int = 2
+    v_ref: float = 0.0
+
+    def c(self) -> L.HelmPml:
+        return L.HelmPml(self.R, self.power, self.v_ref)
+
+
+@dataclasses.dataclass(frozen=True)
+class SolveOpts:
+    k_inner: int = 5
+    max_outer: int = 50
+    rtol: float = 1e-6
+    precond: int = 1
+
+    def c(self) -> L.HelmSolveOpts:
+        return L.HelmSolveOpts(self.k_inner, self.max_outer, self.rtol, self.precond)
+
+
+@dataclasses.dataclass(frozen=True)
+class MlOpts:
+    levels: int = 3
+    ks_o: int = 3
+    ks_i: int = 5
+    kc_o: int = 3
+    kc_i: int = 5
+
+    def c(self) -> L.HelmMlOpts:
+        return L.HelmMlOpts(self.levels, self.ks_o, self.ks_i, self.kc_o, self.kc_i)
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _i64ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def _tptr(t: torch.Tensor):
+    assert t.is_cuda and t.is_contiguous()
+    return C.c_void_p(t.data_ptr())
+
+
+class HelmOp:
+    """Owning handle of a helm_op (helm_setup / helm_destroy)."""
+
+    def __init__(self, handle, grid: Grid, dtype: int, max_rhs: int):
+        self._h = handle
+        self.grid, self.dtype, self.max_rhs = grid, dtype, max_rhs
+        self.tdtype = TORCH_DTYPE[dtype]
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            L.load().helm_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def levels(self) -> List[Tuple[int, int, int]]:
+        lib = L.load()
+        n = C.c_int32()
+        dims = np.zeros((4, 3), np.int64)
+        L.check(lib.helm_levels(self._h, C.byref(n), _i64ptr(dims)))
+        return [tuple(int(v) for v in dims[l]) for l in range(n.value)]
+
+    def get_level(self, level: int, adjoint: int = 0):
+        """Returns (tables[3 axes][3 = lo,dg,up][Nmax] complex128, m_ext (Nz,Ny,Nx) float64)."""
+        lib = L.load()
+        nx, ny, nz = self.levels()[level]
+        nmax = max(nx, ny, nz)
+        tab = np.zeros((3, 3, nmax), np.complex128)
+        m = np.zeros((nz, ny, nx), np.float64)
+        L.check(lib.helm_get_level(self._h, level, adjoint, nmax, tab.ctypes.data_as(C.POINTER(C.c_double)), _dptr(m)))
+        return tab, m
+
+    def workspace_vectors(self) -> float:
+        return L.load().helm_workspace_vectors(self._h)
+
+    def empty(self, nrhs: int = 1, level: int = 0) -> torch.Tensor:
+        nx, ny, nz = self.levels()[level]
+        return torch.empty((nrhs, nz, ny, nx), dtype=self.tdtype, device="cuda")
+
+
+def helm_setup(grid: Grid, m_slowness2: np.ndarray, omega: float, pml: Pml = Pml(), dtype: int = C128,
+               max_rhs: int = 1, mlopts: Optional[MlOpts] = None, stream=None) -> HelmOp:
+    lib = L.load()
+    m = np.ascontiguousarray(m_slowness2, dtype=np.float64)
+    assert m.size == grid.n_interior
+    g, p = grid.c(), pml.c()
+    ml = mlopts.c() if mlopts is not None else None
+    h = C.c_void_p()
+    L.check(lib.helm_setup(C.byref(g), _dptr(m), float(omega), C.byref(p), dtype, max_rhs,
+                           C.byref(ml) if ml is not None else None, _stream(stream), C.byref(h)))
+    return HelmOp(h, grid, dtype, max_rhs)
+
+
+def helm_apply(op: HelmOp, x: torch.Tensor, y: torch.Tensor, adjoint: int = 0, stream=None) -> torch.Tensor:
+    nrhs = x.numel() // op.grid.n_ext
+    assert x.dtype == op.tdtype and y.dtype == op.tdtype and y.numel() == x.numel()
+    L.check(L.load().helm_apply(op.handle, adjoint, nrhs, _tptr(x), _tptr(y), _stream(stream)))
+    return y
+
+
+def helm_solve(op: HelmOp, b: torch.Tensor, x: torch.Tensor, adjoint: int = 0, opts: SolveOpts = SolveOpts(),
+               stream=None) -> List[dict]:
+    nrhs = b.numel() // op.grid.n_ext
+    assert b.dtype == op.tdtype and x.dtype == op.tdtype and x.numel() == b.numel()
+    rep = (L.HelmSolveReport * nrhs)()
+    so = opts.c()
+    L.check(L.load().helm_solve(op.handle, adjoint, nrhs, _tptr(b), _tptr(x), C.byref(so), rep, _stream(stream)))
+    return [r.as_dict() for r in rep]
+
+
+def helm_vcycle(op: HelmOp, b: torch.Tensor, z: torch.Tensor, level: int = 0, adjoint: int = 0, stream=None):
+    nx, ny, nz = op.levels()[level]
+    nrhs = b.numel() // (nx * ny * nz)
+    L.check(L.load().helm_vcycle(op.handle, level, adjoint, nrhs, _tptr(b), _tptr(z), _stream(stream)))
+    return z
+
+
+def helm_transfer(op: HelmOp, inp: torch.Tensor, out: torch.Tensor, level: int = 0, prolong: bool = False,
+                  stream=None):
+    nx, ny, nz = op.levels()[level + (1 if prolong else 0)]
+    nrhs = inp.numel() // (nx * ny * nz)
+    L.check(L.load().helm_transfer(op.handle, level, int(prolong), nrhs, _tptr(inp), _tptr(out), _stream(stream)))
+    return out
+
+
+def _freq_args(freqs, weights):
+    f = np.ascontiguousarray(freqs, np.float64)
+    w = None if weights is None else np.ascontiguousarray(np.asarray(weights, np.complex128).view(np.float64))
+    return f, w
+
+
+def fwi_misfit_grad(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], src_node: np.ndarray,
+                    rec_node: np.ndarray, d_obs: np.ndarray, pml: Pml, dtype: int = C128,
+                    opts: SolveOpts = SolveOpts(), max_rhs: int = 16, src_range: Optional[Tuple[int, int]] = None,
+                    weights=None, fg: Optional[torch.Tensor] = None, stream=None):
+    """Listing 1 `case OBJ`: returns (fg, reports); fg[0] = f, fg[1:] = g (interior, x fastest),
+    fp64 on the device. d_obs: host complex128 (nfreq, nsrc_total, nrec)."""
+    lib = L.load()
+    m = np.ascontiguousarray(m_slowness2, np.float64)
+    src = np.ascontiguousarray(src_node, np.int64)
+    rec = np.ascontiguousarray(rec_node, np.int64)
+    d = np.ascontiguousarray(d_obs, np.complex128)
+    f, w = _freq_args(freqs, weights)
+    s0, s1 = (0, len(src)) if src_range is None else src_range
+    if fg is None:
+        fg = torch.empty(1 + grid.n_interior, dtype=torch.float64, device="cuda")
+    nrep = len(f) * (s1 - s0) * 2
+    rep = (L.HelmSolveReport * max(nrep, 1))()
+    g, p, so = grid.c(), pml.c(), opts.c()
+    L.check(lib.fwi_misfit_grad(C.byref(g), _dptr(m), len(f), _dptr(f), None if w is None else _dptr(w), len(src), s0, s1,
+                                _i64ptr(src), len(rec), _i64ptr(rec), d.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)),
+                                C.byref(p), dtype, C.byref(so), max_rhs, _tptr(fg), rep, _stream(stream)))
+    return fg, [rep[i].as_dict() for i in range(nrep)]
+
+
+def fwi_forward(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], src_node: np.ndarray,
+                rec_node: np.ndarray, pml: Pml, dtype: int = C128, opts: SolveOpts = SolveOpts(), max_rhs: int = 16,
+                src_range: Optional[Tuple[int, int]] = None, weights=None, stream=None):
+    """Listing 1 `case FORW_MODEL`: returns (d (nfreq, ns, nrec) complex128 host, reports)."""
+    lib = L.load()
+    m = np.ascontiguousarray(m_slowness2, np.float64)
+    src = np.ascontiguousarray(src_node, np.int64)
+    rec = np.ascontiguousarray(rec_node, np.int64)
+    f, w = _freq_args(freqs, weights)
+    s0, s1 = (0, len(src)) if src_range is None else src_range
+    d = np.zeros((len(f), s1 - s0, len(rec)), np.complex128)
+    nrep = len(f) * (s1 - s0) * 2
+    rep = (L.HelmSolveReport * max(nrep, 1))()
+    g, p, so = grid.c(), pml.c(), opts.c()
+    L.check(lib.fwi_forward(C.byref(g), _dptr(m), len(f), _dptr(f), None if w is None else _dptr(w), s0, s1,
+                            _i64ptr(src), len(rec), _i64ptr(rec), C.byref(p), dtype, C.byref(so), max_rhs,
+                            d.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), rep, _stream(stream)))
+    return d, [rep[i].as_dict() for i in range(0, nrep, 2)]

@@ -1,0 +1,1014 @@
+// helm.cu — host side of libhelm.so: the helm_op (device-resident model, 1D PML tables,
+// level hierarchy, Krylov workspace), the FGMRES / ML-GMRES orchestration and the C ABI
+// declared in include/helm.h. All numerics run in the kernels of kernels.cuh.
+#include "helm.h"
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+struct HelmErr {
+  helm_status st;
+  std::string msg;
+};
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw HelmErr{e_ == cudaErrorMemoryAllocation ? HELM_ERR_OOM : HELM_ERR_CUDA,       \
+                    std::string(#call) + ": " + cudaGetErrorString(e_)};                  \
+  } while (0)
+#define CKL() CK(cudaGetLastError())
+#define REQ(cond, st, msg) \
+  do {                     \
+    if (!(cond)) throw HelmErr{st, msg}; \
+  } while (0)
+
+constexpr int K1 = HELM_KMAX + 1;
+constexpr int TARGET_BLOCKS = 148 * 8;   // 148 SMs x 8 resident 256-thread CTAs
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return g_num_sms;
+}
+
+template <typename T> T* dalloc(std::vector<void*>& keep, size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  keep.push_back(p);
+  return static_cast<T*>(p);
+}
+
+struct LevelDev {
+  int nx = 0, ny = 0, nz = 0;
+  long long N = 0;
+  double* m64 = nullptr;
+  float* m32 = nullptr;
+  double2* t64[2][3][3] = {};   // [adjoint][axis][lo,dg,up]
+  float2* t32[2][3][3] = {};
+  int tiles = 0;
+};
+
+template <typename R> struct LevelWS {
+  cx<R>* SV[K1] = {};   // smoother basis (GMRES), SV[0] also the V-cycle residual
+  cx<R>* VB = nullptr;  // V-cycle input copy (scaled basis vector of the caller)
+  cx<R>* VX = nullptr;  // level-0 V-cycle output in mixed mode
+  cx<R>* FV[K1] = {};   // coarse-solve basis at this level
+  cx<R>* FZ[HELM_KMAX] = {};
+  cx<R>* Fx = nullptr;
+  cx<R>* Fb = nullptr;
+  KCtx ctxS{}, ctxC{};
+};
+
+}  // namespace
+
+struct helm_op {
+  helm_grid grid{};
+  helm_pml pml{};
+  helm_mlopts ml{};
+  helm_dtype dtype = HELM_C128;
+  int max_rhs = 1;
+  double omega = 0.0;
+  double vref = 0.0;
+  int L = 1;
+  int dim = 3;
+  LevelDev lev[4];
+  LevelWS<double> w64[4];
+  LevelWS<float> w32[4];
+  double2* OV[K1] = {};
+  double2* OZ[HELM_KMAX] = {};
+  double2* OX = nullptr;
+  double2* OB = nullptr;
+  KCtx ctxO{};
+  int* active_d = nullptr;
+  RedBuf rb{};
+  double* m_int_d = nullptr;     // interior model (fp64)
+  std::vector<void*> allocs;
+  cudaStream_t st = nullptr;
+  int k_inner = 5;
+  // accounting (per RHS of the current solve)
+  std::vector<int> act_h;
+  std::vector<double> bytes;
+  std::vector<int64_t> mv[4];
+  double ws_vectors = 0.0;
+  ~helm_op() {
+    for (void* p : allocs) cudaFree(p);
+  }
+};
+
+namespace {
+
+// ------------------------------------------------------------------------------ accounting
+void acct(helm_op* op, int level, double bytes_per_rhs, bool matvec, int nrhs) {
+  for (int r = 0; r < nrhs; ++r)
+    if (op->act_h[r]) {
+      op->bytes[r] += bytes_per_rhs;
+      if (matvec) op->mv[level][r] += 1;
+    }
+}
+
+int blas_blocks(long long N, int nrhs) {
+  long long want = (TARGET_BLOCKS + nrhs - 1) / nrhs;
+  long long cap = (N + HELM_RED_THREADS - 1) / HELM_RED_THREADS;
+  return (int)std::max(1LL, std::min(want, cap));
+}
+
+KCtx make_ctx(std::vector<void*>& keep, int nrhs, int k) {
+  KCtx c{};
+  c.beta = dalloc<double>(keep, nrhs);
+  c.scale = dalloc<double>(keep, (size_t)nrhs * K1);
+  c.H = dalloc<double2>(keep, (size_t)nrhs * K1 * HELM_KMAX);
+  c.cs = dalloc<double>(keep, (size_t)nrhs * HELM_KMAX);
+  c.sn = dalloc<double2>(keep, (size_t)nrhs * HELM_KMAX);
+  c.g = dalloc<double2>(keep, (size_t)nrhs * K1);
+  c.kact = dalloc<int>(keep, nrhs);
+  c.k = k;
+  CK(cudaMemset(c.H, 0, sizeof(double2) * nrhs * K1 * HELM_KMAX));
+  CK(cudaMemset(c.kact, 0, sizeof(int) * nrhs));
+  return c;
+}
+
+template <typename R> Geo<R> geo(const helm_op* op, int l, int adj);
+template <> Geo<double> geo<double>(const helm_op* op, int l, int adj) {
+  const LevelDev& L = op->lev[l];
+  Geo<double> g{};
+  g.nx = L.nx; g.ny = L.ny; g.nz = L.nz; g.N = L.N;
+  g.m = L.m64; g.w2 = op->omega * op->omega;
+  for (int a = 0; a < 3; ++a) { g.lo[a] = L.t64[adj][a][0]; g.dg[a] = L.t64[adj][a][1]; g.up[a] = L.t64[adj][a][2]; }
+  return g;
+}
+template <> Geo<float> geo<float>(const helm_op* op, int l, int adj) {
+  const LevelDev& L = op->lev[l];
+  Geo<float> g{};
+  g.nx = L.nx; g.ny = L.ny; g.nz = L.nz; g.N = L.N;
+  g.m = L.m32; g.w2 = (float)(op->omega * op->omega);
+  for (int a = 0; a < 3; ++a) { g.lo[a] = L.t32[adj][a][0]; g.dg[a] = L.t32[adj][a][1]; g.up[a] = L.t32[adj][a][2]; }
+  return g;
+}
+
+// ------------------------------------------------------------------------------ launchers
+template <typename R>
+void launch_stencil(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* x, cx<R>* y,
+                    const cx<R>* b, const double* xscale, const int* kact, int j, const KCtx& ctx) {
+  const Geo<R> g = geo<R>(op, l, adj);
+  const bool d3 = g.ny > 1;
+  const int BX = d3 ? 32 : 64, BY = d3 ? 8 : 1;
+  const int ntx = (g.nx + BX - 1) / BX, nty = (g.ny + BY - 1) / BY;
+  const long long tiles = (long long)ntx * nty;
+  const int thr_per_blk = BX * BY;
+  long long target = (long long)TARGET_BLOCKS * 256 / thr_per_blk;
+  long long nzc = std::max(1LL, std::min((target + tiles * nrhs - 1) / (tiles * nrhs), (long long)std::max(1, g.nz / 8)));
+  int zlen = (int)((g.nz + nzc - 1) / nzc);
+  nzc = (g.nz + zlen - 1) / zlen;
+  dim3 grid((unsigned)(tiles * nrhs), (unsigned)nzc);
+  const int* act = op->active_d;
+  const size_t S = sizeof(cx<R>);
+  if (d3) {
+    if (mode == 0)
+      k_stencil<R, 32, 8, 0><<<grid, 256, 0, op->st>>>(g, x, y, b, xscale, K1, act, kact, j, nrhs, ntx, nty, zlen, ctx, op->rb);
+    else
+      k_stencil<R, 32, 8, 1><<<grid, 256, 0, op->st>>>(g, x, y, b, xscale, K1, act, kact, j, nrhs, ntx, nty, zlen, ctx, op->rb);
+  } else {
+    if (mode == 0)
+      k_stencil<R, 64, 1, 0><<<grid, 64, 0, op->st>>>(g, x, y, b, xscale, K1, act, kact, j, nrhs, ntx, nty, zlen, ctx, op->rb);
+    else
+      k_stencil<R, 64, 1, 1><<<grid, 64, 0, op->st>>>(g, x, y, b, xscale, K1, act, kact, j, nrhs, ntx, nty, zlen, ctx, op->rb);
+  }
+  CKL();
+  acct(op, l, (mode == 0 ? 2.0 : 3.0) * S * g.N + sizeof(R) * g.N, true, nrhs);
+}
+
+template <typename R> VPtrs<R> vptrs(cx<R>* const* V, const cx<R>* v0, int n) {
+  VPtrs<R> p{};
+  for (int i = 0; i < n && i < K1; ++i) p.p[i] = (i == 0 && v0) ? v0 : V[i];
+  return p;
+}
+
+template <typename R>
+void launch_norm_start(helm_op* op, int l, int nrhs, const cx<R>* b, const KCtx& ctx) {
+  const long long N = op->lev[l].N;
+  dim3 grid(blas_blocks(N, nrhs), nrhs);
+  k_norm_start<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, b, op->active_d, ctx, op->rb);
+  CKL();
+  acct(op, l, sizeof(cx<R>) * (double)N, false, nrhs);
+}
+
+template <typename R>
+void launch_dots(helm_op* op, int l, int nrhs, const VPtrs<R>& V, int j, const cx<R>* w, const KCtx& ctx) {
+  const long long N = op->lev[l].N;
+  dim3 grid(blas_blocks(N, nrhs), nrhs);
+  k_dots<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, V, j, w, op->active_d, ctx, op->rb);
+  CKL();
+  acct(op, l, (j + 2.0) * sizeof(cx<R>) * N, false, nrhs);
+}
+
+template <typename R>
+void launch_update(helm_op* op, int l, int nrhs, const VPtrs<R>& V, int j, cx<R>* w, const KCtx& ctx) {
+  const long long N = op->lev[l].N;
+  dim3 grid(blas_blocks(N, nrhs), nrhs);
+  k_update<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, V, j, w, op->active_d, ctx, op->rb);
+  CKL();
+  acct(op, l, (j + 3.0) * sizeof(cx<R>) * N, false, nrhs);
+}
+
+template <typename R>
+void launch_solupdate(helm_op* op, int l, int nrhs, const VPtrs<R>& Z, const double* zscale, cx<R>* x,
+                      int init, int k, const KCtx& ctx) {
+  const long long N = op->lev[l].N;
+  dim3 grid(blas_blocks(N, nrhs), nrhs);
+  k_solupdate<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, Z, zscale, x, init, op->active_d, ctx);
+  CKL();
+  acct(op, l, (k + (init ? 1.0 : 2.0)) * sizeof(cx<R>) * N, false, nrhs);
+}
+
+template <typename Ti, typename To>
+void launch_copy_scale(helm_op* op, int l, int nrhs, const Ti* in, To* out, const double* scale,
+                       const int* kact, int j) {
+  const long long N = op->lev[l].N;
+  dim3 grid(blas_blocks(N, nrhs), nrhs);
+  k_copy_scale<Ti, To><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, in, out, scale, K1, kact, j, op->active_d);
+  CKL();
+  acct(op, l, (double)(sizeof(Ti) + sizeof(To)) * N, false, nrhs);
+}
+
+template <typename R>
+void launch_restrict(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* out) {
+  const LevelDev &F = op->lev[l], &Cc = op->lev[l + 1];
+  dim3 grid(blas_blocks(Cc.N, nrhs), nrhs);
+  const R fac = (R)std::ldexp(1.0, -op->dim);
+  k_restrict<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3, fac,
+                                                       in, out, op->active_d);
+  CKL();
+  acct(op, l, sizeof(cx<R>) * (double)(F.N + Cc.N), false, nrhs);
+}
+
+template <typename R>
+void launch_prolong_add(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* out) {
+  const LevelDev &F = op->lev[l], &Cc = op->lev[l + 1];
+  dim3 grid(blas_blocks(F.N, nrhs), nrhs);
+  k_prolong_add<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3,
+                                                          in, out, op->active_d);
+  CKL();
+  acct(op, l, sizeof(cx<R>) * (double)(2 * F.N + Cc.N), false, nrhs);
+}
+
+// ------------------------------------------------------------------------------ Krylov
+// One restarted GMRES (flex = false) / FGMRES (flex = true, right preconditioner M) process
+// of `ko` cycles of `ki` Arnoldi steps on level l (fixed counts, R19; breakdown guard D14).
+template <typename R>
+using Precond = std::function<void(const cx<R>* v, const double* vscale, const int* kact, int j, cx<R>* z)>;
+
+template <typename R>
+void krylov(helm_op* op, int l, int adj, int nrhs, KCtx& ctx, int ko, int ki, bool flex, const cx<R>* b,
+            cx<R>* x, bool x0zero, cx<R>* const* V, cx<R>* const* Z, const Precond<R>& M) {
+  ctx.k = ki;
+  for (int cyc = 0; cyc < ko; ++cyc) {
+    const bool first_zero = (cyc == 0 && x0zero);
+    const cx<R>* v0;
+    if (first_zero) {
+      launch_norm_start<R>(op, l, nrhs, b, ctx);
+      v0 = b;
+    } else {
+      launch_stencil<R>(op, l, adj, 1, nrhs, x, V[0], b, nullptr, nullptr, 0, ctx);
+      v0 = V[0];
+    }
+    for (int j = 0; j < ki; ++j) {
+      VPtrs<R> Vp = vptrs<R>(V, v0, j + 1);
+      const cx<R>* zj;
+      const double* zs;
+      if (flex) {
+        M(Vp.p[j], ctx.scale + j, ctx.kact, j, Z[j]);
+        zj = Z[j];
+        zs = nullptr;
+      } else {
+        zj = Vp.p[j];
+        zs = ctx.scale + j;
+      }
+      launch_stencil<R>(op, l, adj, 0, nrhs, zj, V[j + 1], nullptr, zs, ctx.kact, j, ctx);
+      launch_dots<R>(op, l, nrhs, Vp, j, V[j + 1], ctx);
+      launch_update<R>(op, l, nrhs, Vp, j, V[j + 1], ctx);
+    }
+    if (flex) {
+      VPtrs<R> Zp{};
+      for (int i = 0; i < ki; ++i) Zp.p[i] = Z[i];
+      launch_solupdate<R>(op, l, nrhs, Zp, nullptr, x, first_zero, ki, ctx);
+    } else {
+      VPtrs<R> Vp = vptrs<R>(V, v0, ki);
+      launch_solupdate<R>(op, l, nrhs, Vp, ctx.scale, x, first_zero, ki, ctx);
+    }
+  }
+}
+
+template <typename R> LevelWS<R>* wsets(helm_op* op);
+template <> LevelWS<double>* wsets<double>(helm_op* op) { return op->w64; }
+template <> LevelWS<float>* wsets<float>(helm_op* op) { return op->w32; }
+
+// Alg. 1 with the recursion of Fig. 3: x = M_l(b).
+template <typename R>
+void vcycle(helm_op* op, int l, int adj, int nrhs, const cx<R>* b, cx<R>* x) {
+  LevelWS<R>* W = wsets<R>(op);
+  const helm_mlopts& o = op->ml;
+  // pre-smooth: GMRES(ks_o, ks_i) from 0 (R19)
+  krylov<R>(op, l, adj, nrhs, W[l].ctxS, o.ks_o, o.ks_i, false, b, x, true, W[l].SV, nullptr, nullptr);
+  // residual and restriction (R = 2^-d P^T, R21)
+  launch_stencil<R>(op, l, adj, 1, nrhs, x, W[l].SV[0], b, nullptr, nullptr, 0, W[l].ctxS);
+  launch_restrict<R>(op, l, nrhs, W[l].SV[0], W[l + 1].Fb);
+  // coarse solve (R20): coarsest GMRES, otherwise FGMRES preconditioned by V-cycle_{l+1}
+  if (l + 1 == op->L - 1) {
+    krylov<R>(op, l + 1, adj, nrhs, W[l + 1].ctxC, o.kc_o, o.kc_i, false, W[l + 1].Fb, W[l + 1].Fx, true,
+              W[l + 1].FV, nullptr, nullptr);
+  } else {
+    Precond<R> M = [op, l, adj, nrhs, W](const cx<R>* v, const double* vs, const int* kact, int j, cx<R>* z) {
+      launch_copy_scale<cx<R>, cx<R>>(op, l + 1, nrhs, v, W[l + 1].VB, vs, kact, j);
+      vcycle<R>(op, l + 1, adj, nrhs, W[l + 1].VB, z);
+    };
+    krylov<R>(op, l + 1, adj, nrhs, W[l + 1].ctxC, o.kc_o, o.kc_i, true, W[l + 1].Fb, W[l + 1].Fx, true,
+              W[l + 1].FV, W[l + 1].FZ, M);
+  }
+  launch_prolong_add<R>(op, l, nrhs, W[l + 1].Fx, x);
+  // post-smooth: GMRES(ks_o, ks_i) from the current x
+  krylov<R>(op, l, adj, nrhs, W[l].ctxS, o.ks_o, o.ks_i, false, b, x, false, W[l].SV, nullptr, nullptr);
+}
+
+// ------------------------------------------------------------------------------ setup
+void build_tables(helm_op* op) {
+  const helm_grid& G = op->grid;
+  for (int l = 0; l < op->L; ++l) {
+    LevelDev& Lv = op->lev[l];
+    const int Ns[3] = {Lv.nx, Lv.ny, Lv.nz};
+    for (int a = 0; a < 3; ++a) {
+      const int N = Ns[a];
+      if (a == 1 && op->dim == 2) {   // 2D: no y term (tables identically zero)
+        for (int adj = 0; adj < 2; ++adj)
+          for (int t = 0; t < 3; ++t) CK(cudaMemsetAsync(Lv.t64[adj][a][t], 0, sizeof(double2) * N, op->st));
+      } else {
+        AxisPml ap{};
+        ap.N = N; ap.n_int = (int)G.n[a]; ap.wlo = G.pml[a][0]; ap.whi = G.pml[a][1]; ap.level = l;
+        ap.h0 = G.h; ap.omega = op->omega; ap.R = op->pml.R; ap.power = op->pml.power; ap.vref = op->vref;
+        k_tables<<<(N + 127) / 128, 128, 0, op->st>>>(ap, Lv.t64[0][a][0], Lv.t64[0][a][1], Lv.t64[0][a][2]);
+        CKL();
+        k_tables_adj<<<(N + 127) / 128, 128, 0, op->st>>>(N, Lv.t64[0][a][0], Lv.t64[0][a][1], Lv.t64[0][a][2],
+                                                          Lv.t64[1][a][0], Lv.t64[1][a][1], Lv.t64[1][a][2]);
+        CKL();
+      }
+      if (op->dtype == HELM_C64)
+        for (int adj = 0; adj < 2; ++adj)
+          for (int t = 0; t < 3; ++t) {
+            k_cast_c<<<(N + 127) / 128, 128, 0, op->st>>>(N, Lv.t64[adj][a][t], Lv.t32[adj][a][t]);
+            CKL();
+          }
+    }
+  }
+}
+
+void build_models(helm_op* op) {
+  const helm_grid& G = op->grid;
+  LevelDev& L0 = op->lev[0];
+  k_extend<<<(unsigned)((L0.N + 255) / 256), 256, 0, op->st>>>(L0.nx, L0.ny, L0.nz, (int)G.n[0], (int)G.n[1], (int)G.n[2],
+                                                               G.pml[0][0], G.pml[1][0], G.pml[2][0], op->m_int_d, L0.m64);
+  CKL();
+  for (int l = 1; l < op->L; ++l) {
+    const LevelDev &F = op->lev[l - 1];
+    LevelDev& Cc = op->lev[l];
+    k_coarsen_model<<<(unsigned)((Cc.N + 255) / 256), 256, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3,
+                                                                        F.m64, Cc.m64);
+    CKL();
+  }
+  if (op->dtype == HELM_C64)
+    for (int l = 0; l < op->L; ++l) {
+      LevelDev& Lv = op->lev[l];
+      k_cast<double, float><<<(unsigned)((Lv.N + 255) / 256), 256, 0, op->st>>>(Lv.N, Lv.m64, Lv.m32);
+      CKL();
+    }
+}
+
+template <typename R>
+void alloc_ws(helm_op* op) {
+  LevelWS<R>* W = wsets<R>(op);
+  const helm_mlopts& o = op->ml;
+  const int B = op->max_rhs;
+  double vec = 0.0;  // live vectors in units of the finest size
+  const double N0 = (double)op->lev[0].N;
+  for (int l = 0; l < op->L; ++l) {
+    const size_t n = (size_t)op->lev[l].N * B;
+    const double f = op->lev[l].N / N0 * (sizeof(cx<R>) / 16.0);
+    if (l < op->L - 1) {   // levels that run a V-cycle: smoother basis + input copy
+      for (int i = 0; i <= o.ks_i; ++i) W[l].SV[i] = dalloc<cx<R>>(op->allocs, n);
+      W[l].VB = dalloc<cx<R>>(op->allocs, n);
+      W[l].ctxS = make_ctx(op->allocs, B, o.ks_i);
+      vec += (o.ks_i + 2) * f;
+      if (l == 0 && op->dtype == HELM_C64) { W[l].VX = dalloc<cx<R>>(op->allocs, n); vec += f; }
+    }
+    if (l >= 1) {          // coarse solves
+      for (int i = 0; i <= o.kc_i; ++i) W[l].FV[i] = dalloc<cx<R>>(op->allocs, n);
+      const bool flex = (l < op->L - 1);
+      if (flex)
+        for (int i = 0; i < o.kc_i; ++i) W[l].FZ[i] = dalloc<cx<R>>(op->allocs, n);
+      W[l].Fx = dalloc<cx<R>>(op->allocs, n);
+      W[l].Fb = dalloc<cx<R>>(op->allocs, n);
+      W[l].ctxC = make_ctx(op->allocs, B, o.kc_i);
+      vec += ((o.kc_i + 1) + (flex ? o.kc_i : 0) + 2) * f;
+    }
+  }
+  op->ws_vectors += vec;
+}
+
+void validate_grid(const helm_grid* g) {
+  REQ(g, HELM_ERR_ARG, "grid is NULL");
+  REQ(g->ndim == 2 || g->ndim == 3, HELM_ERR_ARG, "ndim must be 2 or 3");
+  REQ(g->h > 0 && std::isfinite(g->h), HELM_ERR_ARG, "h must be > 0");
+  for (int a = 0; a < 3; ++a) {
+    REQ(g->n[a] >= 1, HELM_ERR_SHAPE, "n[a] must be >= 1");
+    REQ(g->pml[a][0] >= 0 && g->pml[a][1] >= 0, HELM_ERR_ARG, "pml widths must be >= 0");
+  }
+  if (g->ndim == 2) REQ(g->n[1] == 1 && g->pml[1][0] == 0 && g->pml[1][1] == 0, HELM_ERR_SHAPE, "2D grids need n[1]=1, pml[1]={0,0}");
+  else REQ(g->n[1] >= 2, HELM_ERR_SHAPE, "3D grids need n[1] >= 2");
+  REQ(g->n[0] >= 2 && g->n[2] >= 2, HELM_ERR_SHAPE, "n[0], n[2] must be >= 2");
+  for (int a = 0; a < 3; ++a) REQ(g->n[a] + g->pml[a][0] + g->pml[a][1] < (1LL << 30), HELM_ERR_SHAPE, "axis too large");
+}
+
+void op_set_model(helm_op* op, const double* m_host) {
+  const helm_grid& G = op->grid;
+  const size_t n_int = (size_t)G.n[0] * G.n[1] * G.n[2];
+  CK(cudaMemcpyAsync(op->m_int_d, m_host, n_int * sizeof(double), cudaMemcpyHostToDevice, op->st));
+  build_models(op);
+}
+
+void op_set_omega(helm_op* op, double omega) {
+  op->omega = omega;
+  build_tables(op);
+}
+
+helm_op* op_create(const helm_grid* grid, const double* m, double omega, const helm_pml* pml, helm_dtype dtype,
+                   int max_rhs, const helm_mlopts* mlo, cudaStream_t st, int k_inner) {
+  validate_grid(grid);
+  REQ(m, HELM_ERR_ARG, "m is NULL");
+  REQ(omega > 0 && std::isfinite(omega), HELM_ERR_ARG, "omega must be > 0");
+  REQ(dtype == HELM_C64 || dtype == HELM_C128, HELM_ERR_ARG, "bad dtype");
+  REQ(max_rhs >= 1, HELM_ERR_ARG, "max_rhs must be >= 1");
+  helm_mlopts o = mlo ? *mlo : helm_mlopts{3, 3, 5, 3, 5};
+  REQ(o.levels >= 1 && o.levels <= 4, HELM_ERR_ARG, "levels must be in [1,4]");
+  REQ(o.ks_o >= 1 && o.ks_i >= 1 && o.kc_o >= 1 && o.kc_i >= 1, HELM_ERR_ARG, "Krylov counts must be >= 1");
+  REQ(o.ks_i <= HELM_KMAX && o.kc_i <= HELM_KMAX && k_inner <= HELM_KMAX && k_inner >= 1, HELM_ERR_ARG,
+      "inner Krylov dimension exceeds HELM_KMAX");
+  helm_pml P = pml ? *pml : helm_pml{1e-4, 2, 0.0};
+  REQ(P.R > 0 && P.R < 1 && P.power >= 0, HELM_ERR_ARG, "bad PML parameters");
+  const size_t n_int = (size_t)grid->n[0] * grid->n[1] * grid->n[2];
+  for (size_t i = 0; i < n_int; ++i) REQ(m[i] > 0 && std::isfinite(m[i]), HELM_ERR_ARG, "m must be > 0 and finite");
+  double vref = P.v_ref;
+  if (!(vref > 0)) {
+    double mmin = m[0];
+    for (size_t i = 1; i < n_int; ++i) mmin = std::min(mmin, m[i]);
+    vref = 1.0 / std::sqrt(mmin);   // max velocity (R5 default)
+  }
+  int dev = 0, major = 0, minor = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  REQ(major == 10 && minor == 0, HELM_ERR_STATE, "libhelm is built for sm_100a (B200) only");
+
+  std::unique_ptr<helm_op> op(new helm_op());
+  op->grid = *grid; op->pml = P; op->ml = o; op->dtype = dtype; op->max_rhs = max_rhs; op->omega = omega;
+  op->vref = vref; op->st = st; op->dim = grid->ndim; op->k_inner = k_inner;
+  // hierarchy sizes (D13): N -> ceil(N/2) on active axes, stop when an axis would be < 5
+  int dims[4][3];
+  dims[0][0] = (int)(grid->n[0] + grid->pml[0][0] + grid->pml[0][1]);
+  dims[0][1] = (int)(grid->n[1] + grid->pml[1][0] + grid->pml[1][1]);
+  dims[0][2] = (int)(grid->n[2] + grid->pml[2][0] + grid->pml[2][1]);
+  int L = 1;
+  while (L < o.levels) {
+    int c[3] = {(dims[L - 1][0] + 1) / 2, op->dim == 3 ? (dims[L - 1][1] + 1) / 2 : 1, (dims[L - 1][2] + 1) / 2};
+    if (c[0] < 5 || c[2] < 5 || (op->dim == 3 && c[1] < 5)) break;
+    for (int a = 0; a < 3; ++a) dims[L][a] = c[a];
+    ++L;
+  }
+  if (L < o.levels) g_err = "warning: grid too small for the requested depth; using " + std::to_string(L) + " levels";
+  op->L = L;
+  for (int l = 0; l < L; ++l) {
+    LevelDev& Lv = op->lev[l];
+    Lv.nx = dims[l][0]; Lv.ny = dims[l][1]; Lv.nz = dims[l][2];
+    Lv.N = (long long)Lv.nx * Lv.ny * Lv.nz;
+    Lv.m64 = dalloc<double>(op->allocs, Lv.N);
+    if (dtype == HELM_C64) Lv.m32 = dalloc<float>(op->allocs, Lv.N);
+    const int Ns[3] = {Lv.nx, Lv.ny, Lv.nz};
+    for (int adj = 0; adj < 2; ++adj)
+      for (int a = 0; a < 3; ++a)
+        for (int t = 0; t < 3; ++t) {
+          Lv.t64[adj][a][t] = dalloc<double2>(op->allocs, Ns[a]);
+          if (dtype == HELM_C64) Lv.t32[adj][a][t] = dalloc<float2>(op->allocs, Ns[a]);
+        }
+  }
+  op->m_int_d = dalloc<double>(op->allocs, n_int);
+  // reduction scratch: stencil residual partials (tiles x z-chunks) or BLAS (KMAX+1) x blocks
+  long long pst = (long long)K1 * TARGET_BLOCKS;
+  for (int l = 0; l < L; ++l) {
+    const LevelDev& Lv = op->lev[l];
+    const bool d3 = Lv.ny > 1;
+    const int BX = d3 ? 32 : 64, BY = d3 ? 8 : 1;
+    long long tiles = (long long)((Lv.nx + BX - 1) / BX) * ((Lv.ny + BY - 1) / BY);
+    pst = std::max(pst, tiles * std::max(1, Lv.nz / 8 + 1));
+  }
+  op->rb.pstride = pst;
+  op->rb.part = dalloc<double2>(op->allocs, (size_t)pst * max_rhs);
+  op->rb.ticket = dalloc<unsigned>(op->allocs, max_rhs);
+  CK(cudaMemset(op->rb.ticket, 0, sizeof(unsigned) * max_rhs));
+  op->active_d = dalloc<int>(op->allocs, max_rhs);
+  // outer FGMRES (always complex128, D15) + V-cycle workspace in the V-cycle precision
+  const size_t n0 = (size_t)op->lev[0].N * max_rhs;
+  for (int i = 0; i <= k_inner; ++i) op->OV[i] = dalloc<double2>(op->allocs, n0);
+  for (int i = 0; i < k_inner; ++i) op->OZ[i] = dalloc<double2>(op->allocs, n0);
+  op->ctxO = make_ctx(op->allocs, max_rhs, k_inner);
+  op->ws_vectors = 2 * k_inner + 1;
+  if (dtype == HELM_C64) {
+    op->OX = dalloc<double2>(op->allocs, n0);
+    op->OB = dalloc<double2>(op->allocs, n0);
+    op->ws_vectors += 2;
+    alloc_ws<float>(op.get());
+  } else {
+    alloc_ws<double>(op.get());
+  }
+  op->act_h.assign(max_rhs, 1);
+  op->bytes.assign(max_rhs, 0.0);
+  for (int l = 0; l < 4; ++l) op->mv[l].assign(max_rhs, 0);
+  op_set_model(op.get(), m);
+  op_set_omega(op.get(), omega);
+  CK(cudaStreamSynchronize(st));
+  return op.release();
+}
+
+void reset_acct(helm_op* op, int nrhs) {
+  std::fill(op->bytes.begin(), op->bytes.end(), 0.0);
+  for (int l = 0; l < 4; ++l) std::fill(op->mv[l].begin(), op->mv[l].end(), 0);
+  std::fill(op->act_h.begin(), op->act_h.end(), 0);
+  std::fill(op->act_h.begin(), op->act_h.begin() + nrhs, 1);
+}
+
+void set_active(helm_op* op, int nrhs) {
+  CK(cudaMemcpyAsync(op->active_d, op->act_h.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, op->st));
+}
+
+// ------------------------------------------------------------------------------ solve
+// Outer FGMRES(k_inner) in complex128 against the fp64 operator (D15), restarted until the
+// TRUE relative residual of every RHS is <= rtol (R23); converged RHS are masked out.
+void solve_c128(helm_op* op, int adj, int nrhs, const double2* B, double2* X, const helm_solve_opts& so,
+                helm_solve_report* rep) {
+  const long long N = op->lev[0].N;
+  reset_acct(op, nrhs);
+  set_active(op, nrhs);
+  CK(cudaMemsetAsync(X, 0, sizeof(double2) * N * nrhs, op->st));
+  KCtx& ctx = op->ctxO;
+  ctx.k = op->k_inner;
+  std::vector<double> bn(nrhs), beta(nrhs), rel(nrhs, 1.0);
+  std::vector<int> cycles(nrhs, 0);
+  launch_norm_start<double>(op, 0, nrhs, B, ctx);
+  CK(cudaMemcpyAsync(bn.data(), ctx.beta, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, op->st));
+  CK(cudaStreamSynchronize(op->st));
+  const bool precond = so.precond != 0 && op->L >= 2;
+  Precond<double> M;
+  if (precond) {
+    if (op->dtype == HELM_C128) {
+      M = [op, adj, nrhs](const double2* v, const double* vs, const int* kact, int j, double2* z) {
+        launch_copy_scale<double2, double2>(op, 0, nrhs, v, op->w64[0].VB, vs, kact, j);
+        vcycle<double>(op, 0, adj, nrhs, op->w64[0].VB, z);
+      };
+    } else {
+      M = [op, adj, nrhs](const double2* v, const double* vs, const int* kact, int j, double2* z) {
+        launch_copy_scale<double2, float2>(op, 0, nrhs, v, op->w32[0].VB, vs, kact, j);
+        vcycle<float>(op, 0, adj, nrhs, op->w32[0].VB, op->w32[0].VX);
+        launch_copy_scale<float2, double2>(op, 0, nrhs, op->w32[0].VX, z, nullptr, nullptr, 0);
+      };
+    }
+  }
+  for (int cyc = 0;; ++cyc) {
+    const double2* v0;
+    if (cyc == 0) {
+      beta = bn;
+      v0 = B;
+    } else {
+      launch_stencil<double>(op, 0, adj, 1, nrhs, X, op->OV[0], B, nullptr, nullptr, 0, ctx);
+      CK(cudaMemcpyAsync(beta.data(), ctx.beta, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, op->st));
+      CK(cudaStreamSynchronize(op->st));
+      v0 = op->OV[0];
+    }
+    int nact = 0;
+    for (int r = 0; r < nrhs; ++r) {
+      if (!op->act_h[r]) continue;
+      rel[r] = bn[r] > 0 ? beta[r] / bn[r] : 0.0;
+      if (rel[r] <= so.rtol || cycles[r] >= so.max_outer) op->act_h[r] = 0;
+      else ++nact;
+    }
+    if (!nact) break;
+    set_active(op, nrhs);
+    const int ki = op->k_inner;
+    for (int j = 0; j < ki; ++j) {
+      VPtrs<double> Vp = vptrs<double>(op->OV, v0, j + 1);
+      const double2* zj;
+      const double* zs;
+      if (precond) {
+        M(Vp.p[j], ctx.scale + j, ctx.kact, j, op->OZ[j]);
+        zj = op->OZ[j];
+        zs = nullptr;
+      } else {
+        zj = Vp.p[j];
+        zs = ctx.scale + j;
+      }
+      launch_stencil<double>(op, 0, adj, 0, nrhs, zj, op->OV[j + 1], nullptr, zs, ctx.kact, j, ctx);
+      launch_dots<double>(op, 0, nrhs, Vp, j, op->OV[j + 1], ctx);
+      launch_update<double>(op, 0, nrhs, Vp, j, op->OV[j + 1], ctx);
+    }
+    if (precond) {
+      VPtrs<double> Zp{};
+      for (int i = 0; i < ki; ++i) Zp.p[i] = op->OZ[i];
+      launch_solupdate<double>(op, 0, nrhs, Zp, nullptr, X, 0, ki, ctx);
+    } else {
+      VPtrs<double> Vp = vptrs<double>(op->OV, v0, ki);
+      launch_solupdate<double>(op, 0, nrhs, Vp, ctx.scale, X, 0, ki, ctx);
+    }
+    for (int r = 0; r < nrhs; ++r)
+      if (op->act_h[r]) cycles[r]++;
+  }
+  CK(cudaStreamSynchronize(op->st));
+  if (rep)
+    for (int r = 0; r < nrhs; ++r) {
+      rep[r].outer_cycles = cycles[r];
+      rep[r].rel_residual = rel[r];
+      rep[r].converged = rel[r] <= so.rtol;
+      for (int l = 0; l < 4; ++l) rep[r].matvecs[l] = op->mv[l][r];
+      rep[r].bytes_alg = op->bytes[r];
+    }
+}
+
+helm_solve_opts default_solve_opts(const helm_op* op) { return helm_solve_opts{op->k_inner, 50, 1e-6, 1}; }
+
+void check_solve_opts(const helm_op* op, const helm_solve_opts& so) {
+  REQ(so.k_inner == op->k_inner, HELM_ERR_ARG, "opts.k_inner must equal the op's k_inner (5)");
+  REQ(so.max_outer >= 0 && so.rtol > 0 && so.rtol < 1, HELM_ERR_ARG, "bad solve options");
+}
+
+void solve_any(helm_op* op, int adj, int nrhs, const void* b, void* x, const helm_solve_opts& so, helm_solve_report* rep) {
+  const long long N = op->lev[0].N;
+  if (op->dtype == HELM_C128) {
+    solve_c128(op, adj, nrhs, (const double2*)b, (double2*)x, so, rep);
+  } else {
+    std::fill(op->act_h.begin(), op->act_h.end(), 1);
+    set_active(op, nrhs);
+    launch_copy_scale<float2, double2>(op, 0, nrhs, (const float2*)b, op->OB, nullptr, nullptr, 0);
+    solve_c128(op, adj, nrhs, op->OB, op->OX, so, rep);
+    std::fill(op->act_h.begin(), op->act_h.end(), 1);
+    set_active(op, nrhs);
+    launch_copy_scale<double2, float2>(op, 0, nrhs, op->OX, (float2*)x, nullptr, nullptr, 0);
+    if (rep)   // the two c64 <-> c128 conversions around the outer solve
+      for (int r = 0; r < nrhs; ++r) rep[r].bytes_alg += 2.0 * 24.0 * N;
+    CK(cudaStreamSynchronize(op->st));
+  }
+}
+
+// ------------------------------------------------------------------------------ FWI
+struct FwiBufs {
+  void *U = nullptr, *V = nullptr, *Bq = nullptr, *A = nullptr;
+  double2* d = nullptr;
+  long long *src_ext = nullptr, *rec_ext = nullptr;
+  double *gext = nullptr, *f = nullptr;
+  std::vector<void*> keep;
+  ~FwiBufs() { for (void* p : keep) cudaFree(p); }
+};
+
+std::vector<long long> to_ext(const helm_grid& G, const int64_t* ids, int n) {
+  std::vector<long long> e(n);
+  const long long nx = G.n[0], ny = G.n[1], nz = G.n[2];
+  const long long Nx = nx + G.pml[0][0] + G.pml[0][1], Ny = ny + G.pml[1][0] + G.pml[1][1];
+  for (int i = 0; i < n; ++i) {
+    REQ(ids[i] >= 0 && ids[i] < nx * ny * nz, HELM_ERR_ARG, "node id out of the interior");
+    long long ix = ids[i] % nx, iy = (ids[i] / nx) % ny, iz = ids[i] / (nx * ny);
+    e[i] = (ix + G.pml[0][0]) + Nx * ((iy + G.pml[1][0]) + Ny * (iz + G.pml[2][0]));
+  }
+  return e;
+}
+
+template <typename R>
+void fwi_run(helm_op* op, const helm_grid& G, int nfreq, const double* freq, const double* sw, int nsrc_total,
+             int s_begin, int s_end, const int64_t* src, int nrec, const int64_t* rec, const double* dobs,
+             const helm_solve_opts& so, double* fg, helm_solve_report* rep, double* d_out, cudaStream_t st) {
+  using C = cx<R>;
+  FwiBufs fb;
+  const long long N = op->lev[0].N;
+  const int B = op->max_rhs;
+  const int ns = s_end - s_begin;
+  fb.U = dalloc<C>(fb.keep, (size_t)N * B);
+  fb.Bq = dalloc<C>(fb.keep, (size_t)N * B);
+  if (!d_out) {
+    fb.V = dalloc<C>(fb.keep, (size_t)N * B);
+    fb.A = dalloc<C>(fb.keep, (size_t)N * B);
+    fb.gext = dalloc<double>(fb.keep, N);
+    fb.f = dalloc<double>(fb.keep, 1);
+    CK(cudaMemsetAsync(fb.gext, 0, sizeof(double) * N, st));
+    CK(cudaMemsetAsync(fb.f, 0, sizeof(double), st));
+  }
+  fb.d = dalloc<double2>(fb.keep, (size_t)B * std::max(nrec, 1));
+  std::vector<long long> sext = to_ext(G, src + s_begin, ns), rext = to_ext(G, rec, nrec);
+  {
+    std::vector<long long> sr = rext;
+    std::sort(sr.begin(), sr.end());
+    REQ(std::adjacent_find(sr.begin(), sr.end()) == sr.end(), HELM_ERR_ARG, "receivers must be distinct nodes");
+  }
+  fb.src_ext = dalloc<long long>(fb.keep, std::max(ns, 1));
+  fb.rec_ext = dalloc<long long>(fb.keep, std::max(nrec, 1));
+  CK(cudaMemcpyAsync(fb.src_ext, sext.data(), sizeof(long long) * ns, cudaMemcpyHostToDevice, st));
+  if (nrec) CK(cudaMemcpyAsync(fb.rec_ext, rext.data(), sizeof(long long) * nrec, cudaMemcpyHostToDevice, st));
+  const double hd = std::pow(G.h, (double)G.ndim);
+  std::vector<helm_solve_report> rtmp(B);
+  for (int fi = 0; fi < nfreq; ++fi) {
+    const double w = 2.0 * M_PI * freq[fi];
+    if (fi > 0 || op->omega != w) op_set_omega(op, w);
+    const double2 S = sw ? make_double2(sw[2 * fi], sw[2 * fi + 1]) : make_double2(1.0, 0.0);
+    const double2 amp = make_double2(S.x / hd, S.y / hd);
+    for (int s0 = 0; s0 < ns; s0 += B) {
+      const int nb = std::min(B, ns - s0);
+      // a7: inject q_s = S e_s / h^d
+      CK(cudaMemsetAsync(fb.Bq, 0, sizeof(C) * N * nb, st));
+      k_inject<R><<<(nb + 127) / 128, 128, 0, st>>>(nb, N, fb.src_ext + s0, amp, (C*)fb.Bq);
+      CKL();
+      // forward solves u = H^-1 q
+      solve_any(op, 0, nb, fb.Bq, fb.U, so, rtmp.data());
+      for (int b = 0; b < nb; ++b)
+        if (rep) rep[((size_t)fi * ns + s0 + b) * 2 + 0] = rtmp[b];
+      if (d_out) {   // FORW_MODEL: d = P_r u
+        if (nrec) {
+          k_gather_data<R><<<(unsigned)((nb * (long long)nrec + 255) / 256), 256, 0, st>>>(nb, nrec, N, fb.rec_ext,
+                                                                                      (const C*)fb.U, fb.d);
+          CKL();
+          CK(cudaMemcpyAsync(d_out + 2 * (((size_t)fi * ns + s0) * nrec), fb.d, sizeof(double2) * nb * nrec,
+                             cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+        }
+        continue;
+      }
+      // a7: r = P_r u - d, f += 1/2 |r|^2, adjoint source -P_r^T r
+      CK(cudaMemcpyAsync(fb.d, dobs + 2 * (((size_t)fi * nsrc_total + s_begin + s0) * nrec),
+                         sizeof(double2) * nb * nrec, cudaMemcpyHostToDevice, st));
+      CK(cudaMemsetAsync(fb.A, 0, sizeof(C) * N * nb, st));
+      dim3 gg(std::max(1, std::min(TARGET_BLOCKS, (nb * nrec + 255) / 256)));
+      k_gather_residual<R><<<gg, HELM_RED_THREADS, 0, st>>>(nb, nrec, N, fb.rec_ext, fb.d, (const C*)fb.U, (C*)fb.A,
+                                                              fb.f, op->rb);
+      CKL();
+      // a8: adjoint solves v = H^-H(-P_r^T r)
+      solve_any(op, 1, nb, fb.A, fb.V, so, rtmp.data());
+      for (int b = 0; b < nb; ++b)
+        if (rep) rep[((size_t)fi * ns + s0 + b) * 2 + 1] = rtmp[b];
+      // a9: g_ext += Re(w^2 conj(u) v)
+      k_grad<R><<<blas_blocks(N, 1), 256, 0, st>>>(nb, N, w * w, (const C*)fb.U, (const C*)fb.V, fb.gext);
+      CKL();
+    }
+  }
+  if (!d_out) {
+    const long long nint = G.n[0] * G.n[1] * G.n[2];
+    k_fold<<<(unsigned)((nint + 255) / 256), 256, 0, st>>>(op->lev[0].nx, op->lev[0].ny, op->lev[0].nz, (int)G.n[0],
+                                                           (int)G.n[1], (int)G.n[2], G.pml[0][0], G.pml[1][0],
+                                                           G.pml[2][0], fb.gext, fb.f, fg);
+    CKL();
+  }
+  CK(cudaStreamSynchronize(st));
+}
+
+// One cached op per thread for fwi_*: the device workspace is reused across calls with the
+// same geometry, dtype and batch size; model, hierarchy and tables are rebuilt every call.
+thread_local helm_op* g_fwi_op = nullptr;
+
+helm_op* fwi_op(const helm_grid* grid, const double* m, double omega, const helm_pml* pml, helm_dtype dtype,
+                int max_rhs, cudaStream_t st) {
+  helm_op* o = g_fwi_op;
+  auto same = [](const helm_grid& a, const helm_grid& b) {
+    if (a.ndim != b.ndim || a.h != b.h) return false;
+    for (int i = 0; i < 3; ++i)
+      if (a.n[i] != b.n[i] || a.pml[i][0] != b.pml[i][0] || a.pml[i][1] != b.pml[i][1]) return false;
+    return true;
+  };
+  if (o && o->dtype == dtype && o->max_rhs == max_rhs && same(o->grid, *grid)) {
+    o->st = st;
+    o->pml = *pml;
+    o->vref = pml->v_ref;
+    op_set_model(o, m);
+    op_set_omega(o, omega);
+    return o;
+  }
+  delete g_fwi_op;
+  g_fwi_op = nullptr;
+  g_fwi_op = op_create(grid, m, omega, pml, dtype, max_rhs, nullptr, st, 5);
+  return g_fwi_op;
+}
+
+helm_status wrap(const std::function<void()>& f) {
+  try {
+    f();
+    return HELM_OK;
+  } catch (const HelmErr& e) {
+    g_err = e.msg;
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return HELM_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HELM_ERR_STATE;
+  }
+}
+
+void* level_ptr_check(const helm_op* op, int level) {
+  REQ(op, HELM_ERR_ARG, "op is NULL");
+  REQ(level >= 0 && level < op->L, HELM_ERR_ARG, "level out of range");
+  return nullptr;
+}
+
+}  // namespace
+
+// ================================================================================ C ABI
+extern "C" {
+
+helm_status helm_setup(const helm_grid* grid, const double* m, double omega, const helm_pml* pml, helm_dtype dtype,
+                       int32_t max_rhs, const helm_mlopts* mlopts, void* stream, helm_op** out) {
+  return wrap([&] {
+    REQ(out, HELM_ERR_ARG, "out is NULL");
+    g_err.clear();
+    *out = op_create(grid, m, omega, pml, dtype, max_rhs, mlopts, (cudaStream_t)stream, 5);
+  });
+}
+
+helm_status helm_apply(helm_op* op, int32_t adjoint, int32_t nrhs, const void* x, void* y, void* stream) {
+  return wrap([&] {
+    REQ(op && x && y, HELM_ERR_ARG, "NULL argument");
+    REQ(nrhs >= 1 && nrhs <= op->max_rhs, HELM_ERR_SHAPE, "nrhs must be in [1, max_rhs]");
+    REQ(adjoint == 0 || adjoint == 1, HELM_ERR_ARG, "adjoint must be 0 or 1");
+    REQ(x != y, HELM_ERR_ARG, "x and y must not alias");
+    op->st = (cudaStream_t)stream;
+    reset_acct(op, nrhs);
+    std::fill(op->act_h.begin(), op->act_h.begin() + nrhs, 1);
+    set_active(op, nrhs);
+    if (op->dtype == HELM_C128)
+      launch_stencil<double>(op, 0, adjoint, 0, nrhs, (const double2*)x, (double2*)y, nullptr, nullptr, nullptr, 0, op->ctxO);
+    else
+      launch_stencil<float>(op, 0, adjoint, 0, nrhs, (const float2*)x, (float2*)y, nullptr, nullptr, nullptr, 0, op->ctxO);
+  });
+}
+
+helm_status helm_solve(helm_op* op, int32_t adjoint, int32_t nrhs, const void* b, void* x, const helm_solve_opts* opts,
+                       helm_solve_report* rep, void* stream) {
+  return wrap([&] {
+    REQ(op && b && x, HELM_ERR_ARG, "NULL argument");
+    REQ(nrhs >= 1 && nrhs <= op->max_rhs, HELM_ERR_SHAPE, "nrhs must be in [1, max_rhs]");
+    REQ(adjoint == 0 || adjoint == 1, HELM_ERR_ARG, "adjoint must be 0 or 1");
+    REQ(b != x, HELM_ERR_ARG, "b and x must not alias");
+    helm_solve_opts so = opts ? *opts : default_solve_opts(op);
+    check_solve_opts(op, so);
+    op->st = (cudaStream_t)stream;
+    solve_any(op, adjoint, nrhs, b, x, so, rep);
+  });
+}
+
+static helm_status fwi_common(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq,
+                              const double* sw, int32_t nsrc_total, int32_t s_begin, int32_t s_end,
+                              const int64_t* src, int32_t nrec, const int64_t* rec, const double* dobs,
+                              const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts, int32_t max_rhs,
+                              double* fg, helm_solve_report* rep, double* d_out, void* stream) {
+  return wrap([&] {
+    validate_grid(grid);
+    REQ(m && freq && src && pml, HELM_ERR_ARG, "NULL argument");
+    REQ(nfreq >= 1, HELM_ERR_ARG, "nfreq must be >= 1");
+    for (int i = 0; i < nfreq; ++i) REQ(freq[i] > 0, HELM_ERR_ARG, "frequencies must be > 0");
+    REQ(pml->v_ref > 0, HELM_ERR_ARG, "fwi requires pml.v_ref > 0 (fixed PML, R31)");
+    REQ(0 <= s_begin && s_begin <= s_end && s_end <= nsrc_total, HELM_ERR_ARG, "bad source range");
+    REQ(nrec >= 0 && (nrec == 0 || rec), HELM_ERR_ARG, "bad receivers");
+    REQ(max_rhs >= 1, HELM_ERR_ARG, "max_rhs must be >= 1");
+    if (!d_out) REQ(fg && (dobs || nrec == 0), HELM_ERR_ARG, "fg / d_obs NULL");
+    const cudaStream_t st = (cudaStream_t)stream;
+    helm_op* op = fwi_op(grid, m, 2.0 * M_PI * freq[0], pml, dtype, max_rhs, st);
+    helm_solve_opts so = opts ? *opts : default_solve_opts(op);
+    check_solve_opts(op, so);
+    if (s_end == s_begin) {   // empty shard: f = 0, g = 0
+      if (!d_out) CK(cudaMemsetAsync(fg, 0, sizeof(double) * (1 + grid->n[0] * grid->n[1] * grid->n[2]), st));
+      CK(cudaStreamSynchronize(st));
+      return;
+    }
+    if (dtype == HELM_C128)
+      fwi_run<double>(op, *grid, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, so, fg, rep, d_out, st);
+    else
+      fwi_run<float>(op, *grid, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, so, fg, rep, d_out, st);
+  });
+}
+
+helm_status fwi_misfit_grad(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq,
+                            const double* sw, int32_t nsrc_total, int32_t s_begin, int32_t s_end, const int64_t* src,
+                            int32_t nrec, const int64_t* rec, const double* dobs, const helm_pml* pml,
+                            helm_dtype dtype, const helm_solve_opts* opts, int32_t max_rhs, double* fg,
+                            helm_solve_report* rep, void* stream) {
+  return fwi_common(grid, m, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, pml, dtype, opts,
+                    max_rhs, fg, rep, nullptr, stream);
+}
+
+helm_status fwi_forward(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq, const double* sw,
+                        int32_t s_begin, int32_t s_end, const int64_t* src, int32_t nrec, const int64_t* rec,
+                        const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts, int32_t max_rhs,
+                        double* d_host, helm_solve_report* rep, void* stream) {
+  if (!d_host) { g_err = "d_host is NULL"; return HELM_ERR_ARG; }
+  return fwi_common(grid, m, nfreq, freq, sw, s_end, s_begin, s_end, src, nrec, rec, nullptr, pml, dtype, opts,
+                    max_rhs, nullptr, rep, d_host, stream);
+}
+
+helm_status helm_levels(const helm_op* op, int32_t* levels, int64_t* dims) {
+  return wrap([&] {
+    REQ(op && levels, HELM_ERR_ARG, "NULL argument");
+    *levels = op->L;
+    if (dims)
+      for (int l = 0; l < op->L; ++l) {
+        dims[3 * l] = op->lev[l].nx; dims[3 * l + 1] = op->lev[l].ny; dims[3 * l + 2] = op->lev[l].nz;
+      }
+  });
+}
+
+helm_status helm_get_level(const helm_op* op, int32_t level, int32_t adjoint, int64_t nmax, double* tables,
+                           double* m_host) {
+  return wrap([&] {
+    level_ptr_check(op, level);
+    REQ(adjoint == 0 || adjoint == 1, HELM_ERR_ARG, "adjoint must be 0 or 1");
+    const LevelDev& Lv = op->lev[level];
+    const int Ns[3] = {Lv.nx, Lv.ny, Lv.nz};
+    REQ(nmax >= *std::max_element(Ns, Ns + 3), HELM_ERR_SHAPE, "nmax smaller than the largest axis");
+    CK(cudaStreamSynchronize(op->st));
+    if (tables) {
+      std::memset(tables, 0, sizeof(double) * 2 * 9 * nmax);
+      for (int a = 0; a < 3; ++a)
+        for (int t = 0; t < 3; ++t)
+          CK(cudaMemcpy(tables + 2 * ((size_t)(a * 3 + t) * nmax), Lv.t64[adjoint][a][t], sizeof(double2) * Ns[a],
+                        cudaMemcpyDeviceToHost));
+    }
+    if (m_host) CK(cudaMemcpy(m_host, Lv.m64, sizeof(double) * Lv.N, cudaMemcpyDeviceToHost));
+  });
+}
+
+helm_status helm_vcycle(helm_op* op, int32_t level, int32_t adjoint, int32_t nrhs, const void* b, void* z, void* stream) {
+  return wrap([&] {
+    level_ptr_check(op, level);
+    REQ(level < op->L - 1, HELM_ERR_ARG, "no V-cycle on the coarsest level");
+    REQ(b && z && b != z, HELM_ERR_ARG, "bad vectors");
+    REQ(nrhs >= 1 && nrhs <= op->max_rhs, HELM_ERR_SHAPE, "nrhs must be in [1, max_rhs]");
+    op->st = (cudaStream_t)stream;
+    reset_acct(op, nrhs);
+    set_active(op, nrhs);
+    if (op->dtype == HELM_C128) {
+      launch_copy_scale<double2, double2>(op, level, nrhs, (const double2*)b, op->w64[level].VB, nullptr, nullptr, 0);
+      vcycle<double>(op, level, adjoint, nrhs, op->w64[level].VB, (double2*)z);
+    } else {
+      launch_copy_scale<float2, float2>(op, level, nrhs, (const float2*)b, op->w32[level].VB, nullptr, nullptr, 0);
+      vcycle<float>(op, level, adjoint, nrhs, op->w32[level].VB, (float2*)z);
+    }
+    CK(cudaStreamSynchronize(op->st));
+  });
+}
+
+helm_status helm_transfer(helm_op* op, int32_t level, int32_t prolong, int32_t nrhs, const void* in, void* out,
+                          void* stream) {
+  return wrap([&] {
+    level_ptr_check(op, level);
+    REQ(level < op->L - 1, HELM_ERR_ARG, "no coarser level");
+    REQ(in && out && in != out, HELM_ERR_ARG, "bad vectors");
+    REQ(nrhs >= 1 && nrhs <= op->max_rhs, HELM_ERR_SHAPE, "nrhs must be in [1, max_rhs]");
+    op->st = (cudaStream_t)stream;
+    reset_acct(op, nrhs);
+    set_active(op, nrhs);
+    if (op->dtype == HELM_C128) {
+      if (prolong) launch_prolong_add<double>(op, level, nrhs, (const double2*)in, (double2*)out);
+      else launch_restrict<double>(op, level, nrhs, (const double2*)in, (double2*)out);
+    } else {
+      if (prolong) launch_prolong_add<float>(op, level, nrhs, (const float2*)in, (float2*)out);
+      else launch_restrict<float>(op, level, nrhs, (const float2*)in, (float2*)out);
+    }
+  });
+}
+
+double helm_workspace_vectors(const helm_op* op) { return op ? op->ws_vectors : 0.0; }
+
+void helm_destroy(helm_op* op) {
+  if (op == g_fwi_op) return;   // the cached FWI op is owned by the library
+  delete op;
+}
+
+const char* helm_last_error(void) { return g_err.c_str(); }
+const char* helm_version(void) { return "libhelm 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,573 @@
+// kernels.cuh — sm_100a kernels of the Helmholtz hot path.
+// Layout: complex interleaved, [rhs][z][y][x] with x fastest on the PML-extended grid.
+// Every reduction is fp64 and deterministic (fixed-order block + last-block ticket).
+#pragma once
+#include "common.cuh"
+
+// ----------------------------------------------------------------------------- geometry
+template <typename R> struct Geo {
+  int nx, ny, nz;          // extended sizes of this level
+  long long N;             // nx*ny*nz
+  const R* m;              // level model (slowness^2), extended
+  R w2;                    // omega^2
+  const cx<R>* lo[3];      // 1D tables of this operator (H or H^H), axis 0=x,1=y,2=z
+  const cx<R>* dg[3];
+  const cx<R>* up[3];
+};
+
+template <typename R> struct VPtrs { const cx<R>* p[HELM_KMAX + 1]; };
+
+struct RedBuf {            // reduction scratch: partials per rhs + one ticket per rhs
+  double2* part;
+  unsigned* ticket;
+  long long pstride;       // double2 entries per rhs
+};
+
+// ================================================================= a1: setup (D2-D4, D6, D13)
+struct AxisPml {
+  int N;            // nodes on this level
+  int n_int;        // interior nodes (finest)
+  int wlo, whi;     // PML widths (finest points)
+  int level;        // coarsening level l (node i at xi = (i 2^l - wlo) h0)
+  double h0, omega, R, power, vref;
+};
+
+__device__ inline double2 pml_eta(double xi, const AxisPml& a) {
+  const double Lint = (a.n_int - 1) * a.h0;
+  double sigma = 0.0;
+  const double c = (a.power + 1.0) * a.vref * log(1.0 / a.R) * 0.5;
+  if (a.wlo > 0) {
+    const double L = a.wlo * a.h0, d = fmax(0.0, -xi);
+    sigma += (c / L) * pow(d / L, a.power);
+  }
+  if (a.whi > 0) {
+    const double L = a.whi * a.h0, d = fmax(0.0, xi - Lint);
+    sigma += (c / L) * pow(d / L, a.power);
+  }
+  return make_double2(1.0, sigma / a.omega);   // eta = 1 + i sigma/omega (R3)
+}
+
+// D4: up_i = 1/(h^2 eta_i eta_{i+1/2}), lo_i = 1/(h^2 eta_i eta_{i-1/2}), dg = -(up+lo).
+// Writes forward tables; the adjoint tables (D6) are derived by k_tables_adj.
+__global__ void k_tables(AxisPml a, double2* lo, double2* dg, double2* up) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  const double s = (double)(1 << a.level);
+  const double h = a.h0 * s;
+  const double xi = ((double)i * s - a.wlo) * a.h0;
+  const double2 e0 = pml_eta(xi, a), ep = pml_eta(xi + 0.5 * h, a), em = pml_eta(xi - 0.5 * h, a);
+  const double2 one = make_double2(1.0 / (h * h), 0.0);
+  double2 pu = make_double2(e0.x * ep.x - e0.y * ep.y, e0.x * ep.y + e0.y * ep.x);
+  double2 pl = make_double2(e0.x * em.x - e0.y * em.y, e0.x * em.y + e0.y * em.x);
+  double2 u = cdiv(one, pu), l = cdiv(one, pl);
+  up[i] = u;
+  lo[i] = l;
+  dg[i] = make_double2(-(u.x + l.x), -(u.y + l.y));
+}
+
+// D6: (T^H y)_i = conj(up_{i-1}) y_{i-1} + conj(dg_i) y_i + conj(lo_{i+1}) y_{i+1}
+__global__ void k_tables_adj(int N, const double2* lo, const double2* dg, const double2* up,
+                             double2* loH, double2* dgH, double2* upH) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  loH[i] = i > 0 ? cconj(up[i - 1]) : make_double2(0.0, 0.0);
+  dgH[i] = cconj(dg[i]);
+  upH[i] = i < N - 1 ? cconj(lo[i + 1]) : make_double2(0.0, 0.0);
+}
+
+// D2: m_ext(i) = m(clamp(i_a - w_a^-, 0, n_a - 1)) (replication along the normal)
+__global__ void k_extend(int Nx, int Ny, int Nz, int nx, int ny, int nz, int wx, int wy, int wz,
+                         const double* __restrict__ m, double* __restrict__ me) {
+  long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (long long)Nx * Ny * Nz) return;
+  int ix = p % Nx, iy = (p / Nx) % Ny, iz = p / ((long long)Nx * Ny);
+  int cx_ = min(max(ix - wx, 0), nx - 1), cy = min(max(iy - wy, 0), ny - 1), cz = min(max(iz - wz, 0), nz - 1);
+  me[p] = m[(long long)cz * nx * ny + (long long)cy * nx + cx_];
+}
+
+// D13: normalized full weighting (1/4, 1/2, 1/4) over in-range fine nodes, per axis.
+__global__ void k_coarsen_model(int fx, int fy, int fz, int cxn, int cyn, int czn, int has_y,
+                                const double* __restrict__ mf, double* __restrict__ mc) {
+  long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (long long)cxn * cyn * czn) return;
+  int jx = p % cxn, jy = (p / cxn) % cyn, jz = p / ((long long)cxn * cyn);
+  double s = 0.0, ws = 0.0;
+  for (int dz = -1; dz <= 1; ++dz) {
+    int iz = 2 * jz + dz;
+    if (iz < 0 || iz >= fz) continue;
+    double wz = dz == 0 ? 0.5 : 0.25;
+    for (int dy = -has_y; dy <= has_y; ++dy) {
+      int iy = has_y ? 2 * jy + dy : 0;
+      if (iy < 0 || iy >= fy) continue;
+      double wy = has_y ? (dy == 0 ? 0.5 : 0.25) : 1.0;
+      for (int dx = -1; dx <= 1; ++dx) {
+        int ix = 2 * jx + dx;
+        if (ix < 0 || ix >= fx) continue;
+        double w = wz * wy * (dx == 0 ? 0.5 : 0.25);
+        s += w * mf[((long long)iz * fy + iy) * fx + ix];
+        ws += w;
+      }
+    }
+  }
+  mc[p] = s / ws;
+}
+
+template <typename Tin, typename Tout>
+__global__ void k_cast(long long n, const Tin* __restrict__ a, Tout* __restrict__ b) {
+  long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) b[p] = (Tout)a[p];
+}
+__global__ void k_cast_c(long long n, const double2* __restrict__ a, float2* __restrict__ b) {
+  long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) b[p] = make_float2((float)a[p].x, (float)a[p].y);
+}
+
+// ================================================================= a2 (+a5, a6): stencil
+// MODE 0: y = s_r * H x                      (s_r = xscale[r*sstride] or 1)
+// MODE 1: y = b - H x, and per-RHS ||y|| starts a Krylov cycle in ctx (beta, v0 scale, g, kact)
+// One CTA owns a BX x BY column tile and a z-range; it marches in z keeping x(z-1), x(z),
+// x(z+1) of its column in registers; the (x, y) neighbours of plane z come from a shared
+// plane with a one-point halo. PML enters only through the 1D tables (D4-D6).
+template <typename R, int BX, int BY, int MODE>
+__global__ void __launch_bounds__(BX * BY)
+k_stencil(Geo<R> g, const cx<R>* __restrict__ x, cx<R>* __restrict__ y, const cx<R>* __restrict__ b,
+          const double* __restrict__ xscale, int sstride, const int* __restrict__ active,
+          const int* __restrict__ kact, int jstep, int nrhs, int ntx, int nty, int zlen,
+          KCtx ctx, RedBuf rb) {
+  using C = cx<R>;
+  const int bid = blockIdx.x;
+  const int r = bid % nrhs, tile = bid / nrhs;
+  if (active && !active[r]) return;
+  if (kact && jstep >= kact[r]) return;
+  const int txb = tile % ntx, tyb = tile / ntx;
+  const int tx = threadIdx.x % BX, ty = threadIdx.x / BX;
+  const int ix = txb * BX + tx, iy = tyb * BY + ty;
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const int z0 = blockIdx.y * zlen, z1 = min(z0 + zlen, nz);
+  const bool valid = ix < nx && iy < ny;
+  const long long N = g.N, plane = (long long)nx * ny;
+  const C* xr = x + (long long)r * N;
+  C* yr = y + (long long)r * N;
+  const C* br = MODE == 1 ? b + (long long)r * N : nullptr;
+  const R s = (MODE == 0 && xscale) ? (R)xscale[(long long)r * sstride] : (R)1;
+  const C zero = mkc((R)0, (R)0);
+
+  __shared__ C sh[BY + 2][BX + 2];
+  C lox = zero, upx = zero, loy = zero, upy = zero, dxy = zero;
+  if (valid) {
+    lox = g.lo[0][ix]; upx = g.up[0][ix];
+    loy = g.lo[1][iy]; upy = g.up[1][iy];
+    dxy = cadd(g.dg[0][ix], g.dg[1][iy]);
+  }
+  const long long col = (long long)iy * nx + ix;
+  auto ld = [&](int xx, int yy, int zz) -> C {
+    if (xx < 0 || xx >= nx || yy < 0 || yy >= ny || zz < 0 || zz >= nz) return zero;
+    return xr[(long long)zz * plane + (long long)yy * nx + xx];
+  };
+  C below = zero, cur = zero, hxl = zero, hxr = zero, hyl = zero, hyr = zero;
+  if (valid) {
+    below = ld(ix, iy, z0 - 1);
+    cur = ld(ix, iy, z0);
+  }
+  if (iy < ny) {
+    if (tx == 0) hxl = ld(ix - 1, iy, z0);
+    if (tx == BX - 1) hxr = ld(ix + 1, iy, z0);
+  }
+  if (ix < nx) {
+    if (ty == 0) hyl = ld(ix, iy - 1, z0);
+    if (ty == BY - 1) hyr = ld(ix, iy + 1, z0);
+  }
+  double nrm = 0.0;
+  for (int z = z0; z < z1; ++z) {
+    // prefetch plane z+1 (centre and halo) into registers
+    C above = zero, nxl = zero, nxr = zero, nyl = zero, nyr = zero;
+    if (valid) above = ld(ix, iy, z + 1);
+    if (z + 1 < z1) {
+      if (iy < ny) {
+        if (tx == 0) nxl = ld(ix - 1, iy, z + 1);
+        if (tx == BX - 1) nxr = ld(ix + 1, iy, z + 1);
+      }
+      if (ix < nx) {
+        if (ty == 0) nyl = ld(ix, iy - 1, z + 1);
+        if (ty == BY - 1) nyr = ld(ix, iy + 1, z + 1);
+      }
+    }
+    sh[ty + 1][tx + 1] = cur;
+    if (tx == 0) sh[ty + 1][0] = hxl;
+    if (tx == BX - 1) sh[ty + 1][BX + 1] = hxr;
+    if (ty == 0) sh[0][tx + 1] = hyl;
+    if (ty == BY - 1) sh[BY + 1][tx + 1] = hyr;
+    __syncthreads();
+    if (valid) {
+      const long long p = (long long)z * plane + col;
+      const C lz = g.lo[2][z], uz = g.up[2][z], dz = g.dg[2][z];
+      const R wm = g.w2 * g.m[p];
+      C dia = mkc(dxy.x + dz.x + wm, dxy.y + dz.y);
+      C acc = cmul(dia, cur);
+      acc = cfma(lox, sh[ty + 1][tx], acc);
+      acc = cfma(upx, sh[ty + 1][tx + 2], acc);
+      acc = cfma(loy, sh[ty][tx + 1], acc);
+      acc = cfma(upy, sh[ty + 2][tx + 1], acc);
+      acc = cfma(lz, below, acc);
+      acc = cfma(uz, above, acc);
+      if (MODE == 0) {
+        yr[p] = cscale(acc, s);
+      } else {
+        C rv = csub(br[p], acc);
+        yr[p] = rv;
+        nrm += (double)rv.x * rv.x + (double)rv.y * rv.y;
+      }
+    }
+    __syncthreads();
+    below = cur; cur = above;
+    hxl = nxl; hxr = nxr; hyl = nyl; hyr = nyr;
+  }
+  if (MODE == 1) {
+    __shared__ double2 sm[32];
+    __shared__ double2 tot[1];
+    double2 v[1] = {make_double2(nrm, 0.0)};
+    const int blk = tile + ntx * nty * blockIdx.y, nblk = ntx * nty * gridDim.y;
+    if (grid_sum_last<1>(v, 1, rb.part + r * rb.pstride, rb.ticket + r, blk, nblk, sm, tot)) {
+      if (threadIdx.x == 0) {
+        const double beta = sqrt(tot[0].x);
+        ctx.beta[r] = beta;
+        ctx.scale[r * (HELM_KMAX + 1)] = beta > 0.0 ? 1.0 / beta : 0.0;
+        for (int i = 0; i <= HELM_KMAX; ++i) ctx.g[r * (HELM_KMAX + 1) + i] = make_double2(i == 0 ? beta : 0.0, 0.0);
+        ctx.kact[r] = beta > 0.0 ? ctx.k : 0;
+      }
+    }
+  }
+}
+
+// ================================================================= a3/a4: Krylov BLAS-1
+// Cycle start from x0 = 0: r = b, v0 = b / ||b|| (lazy: scale only).
+template <typename R>
+__global__ void __launch_bounds__(HELM_RED_THREADS)
+k_norm_start(long long N, const cx<R>* __restrict__ b, const int* __restrict__ active, KCtx ctx, RedBuf rb) {
+  const int r = blockIdx.y;
+  if (active && !active[r]) return;
+  const cx<R>* br = b + (long long)r * N;
+  double s = 0.0;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
+    cx<R> v = br[p];
+    s += (double)v.x * v.x + (double)v.y * v.y;
+  }
+  __shared__ double2 sm[32];
+  __shared__ double2 tot[1];
+  double2 v[1] = {make_double2(s, 0.0)};
+  if (grid_sum_last<1>(v, 1, rb.part + r * rb.pstride, rb.ticket + r, blockIdx.x, gridDim.x, sm, tot)) {
+    if (threadIdx.x == 0) {
+      const double beta = sqrt(tot[0].x);
+      ctx.beta[r] = beta;
+      ctx.scale[r * (HELM_KMAX + 1)] = beta > 0.0 ? 1.0 / beta : 0.0;
+      for (int i = 0; i <= HELM_KMAX; ++i) ctx.g[r * (HELM_KMAX + 1) + i] = make_double2(i == 0 ? beta : 0.0, 0.0);
+      ctx.kact[r] = beta > 0.0 ? ctx.k : 0;
+    }
+  }
+}
+
+// Classical Gram-Schmidt projections h_ij = <v_i, w> = s_i <V_i, w>, i <= j (fp64 sums).
+template <typename R>
+__global__ void __launch_bounds__(HELM_RED_THREADS)
+k_dots(long long N, VPtrs<R> V, int j, const cx<R>* __restrict__ w, const int* __restrict__ active,
+       KCtx ctx, RedBuf rb) {
+  const int r = blockIdx.y;
+  if (active && !active[r]) return;
+  if (j >= ctx.kact[r]) return;
+  const long long off = (long long)r * N;
+  const cx<R>* wr = w + off;
+  double2 acc[HELM_KMAX + 1];
+#pragma unroll
+  for (int i = 0; i <= HELM_KMAX; ++i) acc[i] = make_double2(0.0, 0.0);
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
+    const double2 wv = to_d(wr[p]);
+#pragma unroll
+    for (int i = 0; i <= HELM_KMAX; ++i)
+      if (i <= j) acc[i] = cdot_acc(acc[i], to_d(V.p[i][off + p]), wv);
+  }
+  __shared__ double2 sm[32 * (HELM_KMAX + 1)];
+  __shared__ double2 tot[HELM_KMAX + 1];
+  if (grid_sum_last<HELM_KMAX + 1>(acc, j + 1, rb.part + r * rb.pstride, rb.ticket + r, blockIdx.x, gridDim.x, sm, tot)) {
+    if (threadIdx.x == 0) {
+      const double* sc = ctx.scale + r * (HELM_KMAX + 1);
+      double2* H = ctx.H + (long long)r * (HELM_KMAX + 1) * HELM_KMAX;
+      for (int i = 0; i <= j; ++i) H[hidx(i, j)] = make_double2(tot[i].x * sc[i], tot[i].y * sc[i]);
+    }
+  }
+}
+
+// w <- w - sum_i h_ij v_i (in place, w becomes V_{j+1} unnormalised), ||w||, then (last
+// block) h_{j+1,j}, Givens rotation of column j, residual estimate, breakdown guard (D14).
+template <typename R>
+__global__ void __launch_bounds__(HELM_RED_THREADS)
+k_update(long long N, VPtrs<R> V, int j, cx<R>* __restrict__ w, const int* __restrict__ active,
+         KCtx ctx, RedBuf rb) {
+  const int r = blockIdx.y;
+  if (active && !active[r]) return;
+  if (j >= ctx.kact[r]) return;
+  const long long off = (long long)r * N;
+  cx<R>* wr = w + off;
+  __shared__ cx<R> coef[HELM_KMAX + 1];
+  if (threadIdx.x <= j) {
+    const double2 h = ctx.H[(long long)r * (HELM_KMAX + 1) * HELM_KMAX + hidx(threadIdx.x, j)];
+    const double sc = ctx.scale[r * (HELM_KMAX + 1) + threadIdx.x];
+    coef[threadIdx.x] = from_d<cx<R>>(make_double2(-h.x * sc, -h.y * sc));
+  }
+  __syncthreads();
+  double s = 0.0;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
+    cx<R> wv = wr[p];
+#pragma unroll
+    for (int i = 0; i <= HELM_KMAX; ++i)
+      if (i <= j) wv = cfma(coef[i], V.p[i][off + p], wv);
+    wr[p] = wv;
+    s += (double)wv.x * wv.x + (double)wv.y * wv.y;
+  }
+  __shared__ double2 sm[32];
+  __shared__ double2 tot[1];
+  double2 v[1] = {make_double2(s, 0.0)};
+  if (grid_sum_last<1>(v, 1, rb.part + r * rb.pstride, rb.ticket + r, blockIdx.x, gridDim.x, sm, tot)) {
+    if (threadIdx.x == 0) {
+      const int K1 = HELM_KMAX + 1;
+      double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
+      double* cs = ctx.cs + r * HELM_KMAX;
+      double2* sn = ctx.sn + r * HELM_KMAX;
+      double2* gv = ctx.g + r * K1;
+      const double hn = sqrt(tot[0].x);
+      H[hidx(j + 1, j)] = make_double2(hn, 0.0);
+      for (int i = 0; i < j; ++i) {   // previous rotations
+        const double2 a = H[hidx(i, j)], bb = H[hidx(i + 1, j)];
+        const double c = cs[i];
+        const double2 sv = sn[i];
+        H[hidx(i, j)] = cadd(make_double2(c * a.x, c * a.y), cmul(sv, bb));
+        H[hidx(i + 1, j)] = csub(make_double2(c * bb.x, c * bb.y), cmul(cconj(sv), a));
+      }
+      const double2 a = H[hidx(j, j)];
+      const double bn = hn;
+      const double aa = sqrt(cabs2(a)), rr = sqrt(aa * aa + bn * bn);
+      double c;
+      double2 sv;
+      if (rr == 0.0) { c = 1.0; sv = make_double2(0.0, 0.0); }
+      else if (aa == 0.0) { c = 0.0; sv = make_double2(1.0, 0.0); }
+      else { c = aa / rr; sv = make_double2(a.x / aa * bn / rr, a.y / aa * bn / rr); }
+      cs[j] = c; sn[j] = sv;
+      H[hidx(j, j)] = cadd(make_double2(c * a.x, c * a.y), make_double2(sv.x * bn, sv.y * bn));
+      H[hidx(j + 1, j)] = make_double2(0.0, 0.0);
+      const double2 gj = gv[j];
+      gv[j + 1] = cmul(make_double2(-sv.x, sv.y), gj);   // -conj(s) g_j
+      gv[j] = make_double2(c * gj.x, c * gj.y);
+      if (hn <= 1e-14 * ctx.beta[r]) {                    // breakdown guard (D14)
+        ctx.kact[r] = j + 1;
+        ctx.scale[r * K1 + j + 1] = 0.0;
+      } else {
+        ctx.scale[r * K1 + j + 1] = 1.0 / hn;
+      }
+    }
+  }
+}
+
+// x <- (init ? 0 : x) + sum_{i<kact} y_i z_i with R y = g (back substitution on the rotated
+// Hessenberg, per RHS, recomputed by every block), z_i = zs_i Z_i (zs = lazy scales or 1).
+template <typename R>
+__global__ void __launch_bounds__(HELM_RED_THREADS)
+k_solupdate(long long N, VPtrs<R> Z, const double* __restrict__ zscale, cx<R>* __restrict__ x, int init,
+            const int* __restrict__ active, KCtx ctx) {
+  const int r = blockIdx.y;
+  if (active && !active[r]) return;
+  __shared__ cx<R> yc[HELM_KMAX];
+  __shared__ int s_k;
+  if (threadIdx.x == 0) {
+    const int K1 = HELM_KMAX + 1;
+    const int k = ctx.kact[r];
+    const double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
+    const double2* gv = ctx.g + r * K1;
+    double2 yv[HELM_KMAX];
+    for (int i = k - 1; i >= 0; --i) {
+      double2 t = gv[i];
+      for (int l = i + 1; l < k; ++l) t = csub(t, cmul(H[hidx(i, l)], yv[l]));
+      yv[i] = cdiv(t, H[hidx(i, i)]);
+    }
+    for (int i = 0; i < k; ++i) {
+      const double sc = zscale ? zscale[r * K1 + i] : 1.0;
+      yc[i] = from_d<cx<R>>(make_double2(yv[i].x * sc, yv[i].y * sc));
+    }
+    s_k = k;
+  }
+  __syncthreads();
+  const int k = s_k;
+  if (k == 0 && !init) return;
+  const long long off = (long long)r * N;
+  cx<R>* xr = x + off;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
+    cx<R> xv = init ? mkc((R)0, (R)0) : xr[p];
+#pragma unroll
+    for (int i = 0; i < HELM_KMAX; ++i)
+      if (i < k) xv = cfma(yc[i], Z.p[i][off + p], xv);
+    xr[p] = xv;
+  }
+}
+
+// out = (Tout)(s_r * in); zero if this Krylov step is past the active dimension.
+template <typename Tin, typename Tout>
+__global__ void k_copy_scale(long long N, const Tin* __restrict__ in, Tout* __restrict__ out,
+                             const double* __restrict__ scale, int sstride, const int* __restrict__ kact,
+                             int jstep, const int* __restrict__ active) {
+  const int r = blockIdx.y;
+  if (active && !active[r]) return;
+  const bool dead = kact && jstep >= kact[r];
+  const double s = scale ? scale[(long long)r * sstride] : 1.0;
+  const long long off = (long long)r * N;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
+    double2 v = dead ? make_double2(0.0, 0.0) : to_d(in[off + p]);
+    out[off + p] = from_d<Tout>(make_double2(v.x * s, v.y * s));
+  }
+}
+
+// ================================================================= a5: level transfer (D13)
+// r_c = 2^-d P^T r_f: coarse j gathers fine 2j (weight 1) and 2j+-1 (weight 1/2) per axis.
+template <typename R>
+__global__ void k_restrict(int fx, int fy, int fz, int cxn, int cyn, int czn, int has_y, R fac,
+                           const cx<R>* __restrict__ in, cx<R>* __restrict__ out, const int* __restrict__ active) {
+  const int r = blockIdx.y;
+  if (active && !active[r]) return;
+  const long long Nc = (long long)cxn * cyn * czn, Nf = (long long)fx * fy * fz;
+  const cx<R>* fin = in + (long long)r * Nf;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < Nc; p += (long long)gridDim.x * blockDim.x) {
+    const int jx = p % cxn, jy = (p / cxn) % cyn, jz = p / ((long long)cxn * cyn);
+    cx<R> acc = mkc((R)0, (R)0);
+    for (int dz = -1; dz <= 1; ++dz) {
+      const int iz = 2 * jz + dz;
+      if (iz < 0 || iz >= fz) continue;
+      const R wz = dz == 0 ? (R)1 : (R)0.5;
+      for (int dy = -has_y; dy <= has_y; ++dy) {
+        const int iy = has_y ? 2 * jy + dy : 0;
+        if (iy < 0 || iy >= fy) continue;
+        const R wy = wz * (dy == 0 ? (R)1 : (R)0.5);
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int ix = 2 * jx + dx;
+          if (ix < 0 || ix >= fx) continue;
+          const R w = wy * (dx == 0 ? (R)1 : (R)0.5);
+          const cx<R> v = fin[((long long)iz * fy + iy) * fx + ix];
+          acc.x += w * v.x;
+          acc.y += w * v.y;
+        }
+      }
+    }
+    out[(long long)r * Nc + p] = mkc(acc.x * fac, acc.y * fac);
+  }
+}
+
+// x_f += P x_c: fine 2j <- c_j; fine 2j+1 <- (c_j + c_{j+1})/2 with c_{Nc} = 0, tensor product.
+template <typename R>
+__global__ void k_prolong_add(int fx, int fy, int fz, int cxn, int cyn, int czn, int has_y,
+                              const cx<R>* __restrict__ in, cx<R>* __restrict__ out, const int* __restrict__ active) {
+  const int r = blockIdx.y;
+  if (active && !active[r]) return;
+  const long long Nc = (long long)cxn * cyn * czn, Nf = (long long)fx * fy * fz;
+  const cx<R>* cin = in + (long long)r * Nc;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < Nf; p += (long long)gridDim.x * blockDim.x) {
+    const int ix = p % fx, iy = (p / fx) % fy, iz = p / ((long long)fx * fy);
+    int jx[2], jy[2], jz[2];
+    R wx[2], wy[2], wz[2];
+    int nxp, nyp, nzp;
+    auto axis = [](int i, int nc, int* j, R* w, int& n) {
+      if ((i & 1) == 0) { j[0] = i >> 1; w[0] = (R)1; n = 1; }
+      else { j[0] = i >> 1; w[0] = (R)0.5; j[1] = (i >> 1) + 1; w[1] = (R)0.5; n = j[1] < nc ? 2 : 1; }
+    };
+    axis(ix, cxn, jx, wx, nxp);
+    axis(iz, czn, jz, wz, nzp);
+    if (has_y) axis(iy, cyn, jy, wy, nyp);
+    else { jy[0] = 0; wy[0] = (R)1; nyp = 1; }
+    cx<R> acc = mkc((R)0, (R)0);
+    for (int a = 0; a < nzp; ++a)
+      for (int bq = 0; bq < nyp; ++bq)
+        for (int c = 0; c < nxp; ++c) {
+          const R w = wz[a] * wy[bq] * wx[c];
+          const cx<R> v = cin[((long long)jz[a] * cyn + jy[bq]) * cxn + jx[c]];
+          acc.x += w * v.x;
+          acc.y += w * v.y;
+        }
+    cx<R>* o = out + (long long)r * Nf + p;
+    *o = cadd(*o, acc);
+  }
+}
+
+// ================================================================= a7, a9: FWI kernels
+// q_s = S e_node(s) / h^d (D7); B zeroed beforehand.
+template <typename R>
+__global__ void k_inject(int ns, long long N, const long long* __restrict__ src_ext, double2 amp, cx<R>* __restrict__ B) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < ns) B[(long long)s * N + src_ext[s]] = from_d<cx<R>>(amp);
+}
+
+// r = P_r u - d (D8, D10); A = -P_r^T r (D11, receivers distinct); f += 1/2 ||r||^2 (fp64,
+// deterministic: block partials + last-block ticket, then one sequential add into *f).
+template <typename R>
+__global__ void __launch_bounds__(HELM_RED_THREADS)
+k_gather_residual(int ns, int nrec, long long N, const long long* __restrict__ rec_ext,
+                  const double2* __restrict__ d, const cx<R>* __restrict__ U, cx<R>* __restrict__ A,
+                  double* f, RedBuf rb) {
+  double s = 0.0;
+  const long long tot_n = (long long)ns * nrec;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < tot_n; q += (long long)gridDim.x * blockDim.x) {
+    const int si = q / nrec, k = q % nrec;
+    const long long e = rec_ext[k];
+    const double2 u = to_d(U[(long long)si * N + e]);
+    const double2 rv = csub(u, d[q]);
+    A[(long long)si * N + e] = from_d<cx<R>>(make_double2(-rv.x, -rv.y));
+    s += cabs2(rv);
+  }
+  __shared__ double2 sm[32];
+  __shared__ double2 tot[1];
+  double2 v[1] = {make_double2(s, 0.0)};
+  if (grid_sum_last<1>(v, 1, rb.part, rb.ticket, blockIdx.x, gridDim.x, sm, tot)) {
+    if (threadIdx.x == 0) *f += 0.5 * tot[0].x;
+  }
+}
+
+// d[s][k] = (P_r u_s)_k (D8; Listing 1 FORW_MODEL P:164-165)
+template <typename R>
+__global__ void k_gather_data(int ns, int nrec, long long N, const long long* __restrict__ rec_ext,
+                              const cx<R>* __restrict__ U, double2* __restrict__ d) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)ns * nrec) return;
+  const int si = q / nrec, k = q % nrec;
+  d[q] = to_d(U[(long long)si * N + rec_ext[k]]);
+}
+
+// g_ext += sum_s Re(omega^2 conj(u_s) v_s) (Eq. 8, Listing 1), fp64.
+template <typename R>
+__global__ void k_grad(int ns, long long N, double w2, const cx<R>* __restrict__ U, const cx<R>* __restrict__ V,
+                       double* __restrict__ gext) {
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < ns; ++s) {
+      const double2 u = to_d(U[(long long)s * N + p]), v = to_d(V[(long long)s * N + p]);
+      acc += u.x * v.x + u.y * v.y;
+    }
+    gext[p] += w2 * acc;
+  }
+}
+
+// g = E^T g_ext (D12, R11): each interior cell sums the extended nodes that replicate it
+// (its PML line / face / corner box); written into fg[1 + i]; fg[0] = f.
+__global__ void k_fold(int Nx, int Ny, int Nz, int nx, int ny, int nz, int wx, int wy, int wz,
+                       const double* __restrict__ gext, const double* __restrict__ f, double* __restrict__ fg) {
+  long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p == 0) fg[0] = *f;
+  if (p >= (long long)nx * ny * nz) return;
+  const int ix = p % nx, iy = (p / nx) % ny, iz = p / ((long long)nx * ny);
+  auto range = [](int i, int n, int w, int Nn, int& a, int& b) {
+    a = i == 0 ? 0 : i + w;
+    b = i == n - 1 ? Nn - 1 : i + w;
+  };
+  int xa, xb, ya, yb, za, zb;
+  range(ix, nx, wx, Nx, xa, xb);
+  range(iy, ny, wy, Ny, ya, yb);
+  range(iz, nz, wz, Nz, za, zb);
+  double s = 0.0;
+  for (int k = za; k <= zb; ++k)
+    for (int j = ya; j <= yb; ++j)
+      for (int i = xa; i <= xb; ++i) s += gext[((long long)k * Ny + j) * Nx + i];
+  fg[1 + p] = s;
+}
