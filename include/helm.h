@@ -150,6 +150,25 @@ helm_status helm_vcycle(helm_op* op, int32_t level, int32_t adjoint, int32_t nrh
 helm_status helm_transfer(helm_op* op, int32_t level, int32_t prolong, int32_t nrhs,
                           const void* in_dev, void* out_dev, void* cuda_stream);
 
+/* ---- measurement probes (bench.py) ---------------------------------------------------- */
+
+/* Kernel classes: 0 stencil (y = H x), 1 stencil-residual (r = b - H x, ||r||), 2 norm,
+ * 3 dots (CGS projections), 4 update (+norm, Givens), 5 solution update, 6 copy/convert,
+ * 7 restrict, 8 prolong-add, 9 fwi (inject/gather/gradient/fold), 10 setup. */
+#define HELM_NCLASS 11
+
+/* When enable != 0, every `stride`-th launch of each class is bracketed by CUDA events
+ * recorded on the stream it is launched on. Resets the accumulated statistics. */
+helm_status helm_profile(int32_t enable, int32_t stride);
+
+/* Per class (arrays of HELM_NCLASS): launches since the last helm_profile call, sampled
+ * launches, summed device ms of the sampled launches, summed algorithmic bytes of the
+ * sampled launches. Synchronizes on the recorded events. */
+helm_status helm_profile_read(int64_t* launches, int64_t* sampled, double* ms, double* bytes);
+
+/* Total kernel launches issued by this library since it was loaded. */
+int64_t     helm_launch_count(void);
+
 /* Peak live workspace of a solve, in vectors of the finest size per RHS. */
 double      helm_workspace_vectors(const helm_op* op);
 

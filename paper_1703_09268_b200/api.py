@@ -241,3 +241,25 @@ def fwi_forward(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], src
                             _i64ptr(src), len(rec), _i64ptr(rec), C.byref(p), dtype, C.byref(so), max_rhs,
                             d.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), rep, _stream(stream)))
     return d, [rep[i].as_dict() for i in range(0, nrep, 2)]
+
+
+# ---------------------------------------------------------------------------- measurement
+def profile(enable: bool, stride: int = 1):
+    """Sample every `stride`-th launch of each kernel class with CUDA events on its stream."""
+    L.check(L.load().helm_profile(int(enable), int(stride)))
+
+
+def profile_read() -> dict:
+    lib = L.load()
+    n = L.NCLASS
+    la = np.zeros(n, np.int64)
+    sa = np.zeros(n, np.int64)
+    ms = np.zeros(n)
+    by = np.zeros(n)
+    L.check(lib.helm_profile_read(_i64ptr(la), _i64ptr(sa), _dptr(ms), _dptr(by)))
+    return {L.CLASS_NAMES[c]: {"launches": int(la[c]), "sampled": int(sa[c]), "ms": float(ms[c]),
+                               "bytes": float(by[c])} for c in range(n)}
+
+
+def launch_count() -> int:
+    return int(L.load().helm_launch_count())

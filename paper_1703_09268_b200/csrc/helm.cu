@@ -36,6 +36,72 @@ struct HelmErr {
   } while (0)
 
 constexpr int K1 = HELM_KMAX + 1;
+
+// ------------------------------------------------------------------------------ probes
+enum KClass { KC_STENCIL = 0, KC_RESID, KC_NORM, KC_DOTS, KC_UPDATE, KC_SOLUPD, KC_COPY, KC_RESTRICT,
+              KC_PROLONG, KC_FWI, KC_SETUP };
+struct ProbeRec { int cls; cudaEvent_t a, b; double bytes; };
+struct Prof {
+  bool on = false;
+  int stride = 1;
+  long long launches[HELM_NCLASS] = {};
+  long long sampled[HELM_NCLASS] = {};
+  double ms[HELM_NCLASS] = {};
+  double bytes[HELM_NCLASS] = {};
+  std::vector<ProbeRec> pending;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t cur_a = nullptr;
+  bool cur_sampled = false;
+};
+Prof g_prof;
+long long g_launches = 0;
+
+cudaEvent_t prof_event() {
+  if (!g_prof.pool.empty()) {
+    cudaEvent_t e = g_prof.pool.back();
+    g_prof.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+// Launch counted but never timed (setup / FWI bookkeeping kernels).
+inline void prof_count(int cls) {
+  ++g_launches;
+  if (g_prof.on) g_prof.launches[cls]++;
+}
+// Call immediately before a launch on stream st.
+inline void prof_begin(int cls, cudaStream_t st) {
+  ++g_launches;
+  if (!g_prof.on) return;
+  g_prof.cur_sampled = (g_prof.launches[cls]++ % g_prof.stride) == 0;
+  if (g_prof.cur_sampled) {
+    g_prof.cur_a = prof_event();
+    cudaEventRecord(g_prof.cur_a, st);
+  }
+}
+// Call immediately after the launch, with its algorithmic bytes (all RHS).
+inline void prof_end(int cls, cudaStream_t st, double bytes) {
+  if (!g_prof.on || !g_prof.cur_sampled) return;
+  cudaEvent_t b = prof_event();
+  cudaEventRecord(b, st);
+  g_prof.pending.push_back({cls, g_prof.cur_a, b, bytes});
+  g_prof.cur_sampled = false;
+}
+void prof_drain() {
+  for (auto& r : g_prof.pending) {
+    cudaEventSynchronize(r.b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    g_prof.ms[r.cls] += t;
+    g_prof.bytes[r.cls] += r.bytes;
+    g_prof.sampled[r.cls] += 1;
+    g_prof.pool.push_back(r.a);
+    g_prof.pool.push_back(r.b);
+  }
+  g_prof.pending.clear();
+}
 constexpr int TARGET_BLOCKS = 148 * 8;   // 148 SMs x 8 resident 256-thread CTAs
 
 int g_num_sms = 0;
@@ -116,12 +182,15 @@ struct helm_op {
 namespace {
 
 // ------------------------------------------------------------------------------ accounting
-void acct(helm_op* op, int level, double bytes_per_rhs, bool matvec, int nrhs) {
+double acct(helm_op* op, int level, double bytes_per_rhs, bool matvec, int nrhs) {
+  double tot = 0.0;
   for (int r = 0; r < nrhs; ++r)
     if (op->act_h[r]) {
       op->bytes[r] += bytes_per_rhs;
+      tot += bytes_per_rhs;
       if (matvec) op->mv[level][r] += 1;
     }
+  return tot;
 }
 
 int blas_blocks(long long N, int nrhs) {
@@ -180,6 +249,8 @@ void launch_stencil(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>
   dim3 grid((unsigned)(tiles * nrhs), (unsigned)nzc);
   const int* act = op->active_d;
   const size_t S = sizeof(cx<R>);
+  const int cls = mode ? KC_RESID : KC_STENCIL;
+  prof_begin(cls, op->st);
   if (d3) {
     if (mode == 0)
       k_stencil<R, 32, 8, 0><<<grid, 256, 0, op->st>>>(g, x, y, b, xscale, K1, act, kact, j, nrhs, ntx, nty, zlen, ctx, op->rb);
@@ -192,7 +263,7 @@ void launch_stencil(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>
       k_stencil<R, 64, 1, 1><<<grid, 64, 0, op->st>>>(g, x, y, b, xscale, K1, act, kact, j, nrhs, ntx, nty, zlen, ctx, op->rb);
   }
   CKL();
-  acct(op, l, (mode == 0 ? 2.0 : 3.0) * S * g.N + sizeof(R) * g.N, true, nrhs);
+  prof_end(cls, op->st, acct(op, l, (mode == 0 ? 2.0 : 3.0) * S * g.N + sizeof(R) * g.N, true, nrhs));
 }
 
 template <typename R> VPtrs<R> vptrs(cx<R>* const* V, const cx<R>* v0, int n) {
@@ -205,27 +276,30 @@ template <typename R>
 void launch_norm_start(helm_op* op, int l, int nrhs, const cx<R>* b, const KCtx& ctx) {
   const long long N = op->lev[l].N;
   dim3 grid(blas_blocks(N, nrhs), nrhs);
+  prof_begin(KC_NORM, op->st);
   k_norm_start<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, b, op->active_d, ctx, op->rb);
   CKL();
-  acct(op, l, sizeof(cx<R>) * (double)N, false, nrhs);
+  prof_end(KC_NORM, op->st, acct(op, l, sizeof(cx<R>) * (double)N, false, nrhs));
 }
 
 template <typename R>
 void launch_dots(helm_op* op, int l, int nrhs, const VPtrs<R>& V, int j, const cx<R>* w, const KCtx& ctx) {
   const long long N = op->lev[l].N;
   dim3 grid(blas_blocks(N, nrhs), nrhs);
+  prof_begin(KC_DOTS, op->st);
   k_dots<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, V, j, w, op->active_d, ctx, op->rb);
   CKL();
-  acct(op, l, (j + 2.0) * sizeof(cx<R>) * N, false, nrhs);
+  prof_end(KC_DOTS, op->st, acct(op, l, (j + 2.0) * sizeof(cx<R>) * N, false, nrhs));
 }
 
 template <typename R>
 void launch_update(helm_op* op, int l, int nrhs, const VPtrs<R>& V, int j, cx<R>* w, const KCtx& ctx) {
   const long long N = op->lev[l].N;
   dim3 grid(blas_blocks(N, nrhs), nrhs);
+  prof_begin(KC_UPDATE, op->st);
   k_update<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, V, j, w, op->active_d, ctx, op->rb);
   CKL();
-  acct(op, l, (j + 3.0) * sizeof(cx<R>) * N, false, nrhs);
+  prof_end(KC_UPDATE, op->st, acct(op, l, (j + 3.0) * sizeof(cx<R>) * N, false, nrhs));
 }
 
 template <typename R>
@@ -233,9 +307,10 @@ void launch_solupdate(helm_op* op, int l, int nrhs, const VPtrs<R>& Z, const dou
                       int init, int k, const KCtx& ctx) {
   const long long N = op->lev[l].N;
   dim3 grid(blas_blocks(N, nrhs), nrhs);
+  prof_begin(KC_SOLUPD, op->st);
   k_solupdate<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, Z, zscale, x, init, op->active_d, ctx);
   CKL();
-  acct(op, l, (k + (init ? 1.0 : 2.0)) * sizeof(cx<R>) * N, false, nrhs);
+  prof_end(KC_SOLUPD, op->st, acct(op, l, (k + (init ? 1.0 : 2.0)) * sizeof(cx<R>) * N, false, nrhs));
 }
 
 template <typename Ti, typename To>
@@ -243,9 +318,10 @@ void launch_copy_scale(helm_op* op, int l, int nrhs, const Ti* in, To* out, cons
                        const int* kact, int j) {
   const long long N = op->lev[l].N;
   dim3 grid(blas_blocks(N, nrhs), nrhs);
+  prof_begin(KC_COPY, op->st);
   k_copy_scale<Ti, To><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, in, out, scale, K1, kact, j, op->active_d);
   CKL();
-  acct(op, l, (double)(sizeof(Ti) + sizeof(To)) * N, false, nrhs);
+  prof_end(KC_COPY, op->st, acct(op, l, (double)(sizeof(Ti) + sizeof(To)) * N, false, nrhs));
 }
 
 template <typename R>
@@ -253,20 +329,22 @@ void launch_restrict(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* out) 
   const LevelDev &F = op->lev[l], &Cc = op->lev[l + 1];
   dim3 grid(blas_blocks(Cc.N, nrhs), nrhs);
   const R fac = (R)std::ldexp(1.0, -op->dim);
+  prof_begin(KC_RESTRICT, op->st);
   k_restrict<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3, fac,
                                                        in, out, op->active_d);
   CKL();
-  acct(op, l, sizeof(cx<R>) * (double)(F.N + Cc.N), false, nrhs);
+  prof_end(KC_RESTRICT, op->st, acct(op, l, sizeof(cx<R>) * (double)(F.N + Cc.N), false, nrhs));
 }
 
 template <typename R>
 void launch_prolong_add(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* out) {
   const LevelDev &F = op->lev[l], &Cc = op->lev[l + 1];
   dim3 grid(blas_blocks(F.N, nrhs), nrhs);
+  prof_begin(KC_PROLONG, op->st);
   k_prolong_add<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3,
                                                           in, out, op->active_d);
   CKL();
-  acct(op, l, sizeof(cx<R>) * (double)(2 * F.N + Cc.N), false, nrhs);
+  prof_end(KC_PROLONG, op->st, acct(op, l, sizeof(cx<R>) * (double)(2 * F.N + Cc.N), false, nrhs));
 }
 
 // ------------------------------------------------------------------------------ Krylov
@@ -362,8 +440,10 @@ void build_tables(helm_op* op) {
         AxisPml ap{};
         ap.N = N; ap.n_int = (int)G.n[a]; ap.wlo = G.pml[a][0]; ap.whi = G.pml[a][1]; ap.level = l;
         ap.h0 = G.h; ap.omega = op->omega; ap.R = op->pml.R; ap.power = op->pml.power; ap.vref = op->vref;
+        prof_count(KC_SETUP);
         k_tables<<<(N + 127) / 128, 128, 0, op->st>>>(ap, Lv.t64[0][a][0], Lv.t64[0][a][1], Lv.t64[0][a][2]);
         CKL();
+        prof_count(KC_SETUP);
         k_tables_adj<<<(N + 127) / 128, 128, 0, op->st>>>(N, Lv.t64[0][a][0], Lv.t64[0][a][1], Lv.t64[0][a][2],
                                                           Lv.t64[1][a][0], Lv.t64[1][a][1], Lv.t64[1][a][2]);
         CKL();
@@ -371,6 +451,7 @@ void build_tables(helm_op* op) {
       if (op->dtype == HELM_C64)
         for (int adj = 0; adj < 2; ++adj)
           for (int t = 0; t < 3; ++t) {
+            prof_count(KC_SETUP);
             k_cast_c<<<(N + 127) / 128, 128, 0, op->st>>>(N, Lv.t64[adj][a][t], Lv.t32[adj][a][t]);
             CKL();
           }
@@ -381,12 +462,14 @@ void build_tables(helm_op* op) {
 void build_models(helm_op* op) {
   const helm_grid& G = op->grid;
   LevelDev& L0 = op->lev[0];
+  prof_count(KC_SETUP);
   k_extend<<<(unsigned)((L0.N + 255) / 256), 256, 0, op->st>>>(L0.nx, L0.ny, L0.nz, (int)G.n[0], (int)G.n[1], (int)G.n[2],
                                                                G.pml[0][0], G.pml[1][0], G.pml[2][0], op->m_int_d, L0.m64);
   CKL();
   for (int l = 1; l < op->L; ++l) {
     const LevelDev &F = op->lev[l - 1];
     LevelDev& Cc = op->lev[l];
+    prof_count(KC_SETUP);
     k_coarsen_model<<<(unsigned)((Cc.N + 255) / 256), 256, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3,
                                                                         F.m64, Cc.m64);
     CKL();
@@ -394,6 +477,7 @@ void build_models(helm_op* op) {
   if (op->dtype == HELM_C64)
     for (int l = 0; l < op->L; ++l) {
       LevelDev& Lv = op->lev[l];
+      prof_count(KC_SETUP);
       k_cast<double, float><<<(unsigned)((Lv.N + 255) / 256), 256, 0, op->st>>>(Lv.N, Lv.m64, Lv.m32);
       CKL();
     }
@@ -743,6 +827,7 @@ void fwi_run(helm_op* op, const helm_grid& G, int nfreq, const double* freq, con
       const int nb = std::min(B, ns - s0);
       // a7: inject q_s = S e_s / h^d
       CK(cudaMemsetAsync(fb.Bq, 0, sizeof(C) * N * nb, st));
+      prof_count(KC_FWI);
       k_inject<R><<<(nb + 127) / 128, 128, 0, st>>>(nb, N, fb.src_ext + s0, amp, (C*)fb.Bq);
       CKL();
       // forward solves u = H^-1 q
@@ -751,6 +836,7 @@ void fwi_run(helm_op* op, const helm_grid& G, int nfreq, const double* freq, con
         if (rep) rep[((size_t)fi * ns + s0 + b) * 2 + 0] = rtmp[b];
       if (d_out) {   // FORW_MODEL: d = P_r u
         if (nrec) {
+          prof_count(KC_FWI);
           k_gather_data<R><<<(unsigned)((nb * (long long)nrec + 255) / 256), 256, 0, st>>>(nb, nrec, N, fb.rec_ext,
                                                                                       (const C*)fb.U, fb.d);
           CKL();
@@ -765,6 +851,7 @@ void fwi_run(helm_op* op, const helm_grid& G, int nfreq, const double* freq, con
                          sizeof(double2) * nb * nrec, cudaMemcpyHostToDevice, st));
       CK(cudaMemsetAsync(fb.A, 0, sizeof(C) * N * nb, st));
       dim3 gg(std::max(1, std::min(TARGET_BLOCKS, (nb * nrec + 255) / 256)));
+      prof_count(KC_FWI);
       k_gather_residual<R><<<gg, HELM_RED_THREADS, 0, st>>>(nb, nrec, N, fb.rec_ext, fb.d, (const C*)fb.U, (C*)fb.A,
                                                               fb.f, op->rb);
       CKL();
@@ -773,12 +860,14 @@ void fwi_run(helm_op* op, const helm_grid& G, int nfreq, const double* freq, con
       for (int b = 0; b < nb; ++b)
         if (rep) rep[((size_t)fi * ns + s0 + b) * 2 + 1] = rtmp[b];
       // a9: g_ext += Re(w^2 conj(u) v)
+      prof_count(KC_FWI);
       k_grad<R><<<blas_blocks(N, 1), 256, 0, st>>>(nb, N, w * w, (const C*)fb.U, (const C*)fb.V, fb.gext);
       CKL();
     }
   }
   if (!d_out) {
     const long long nint = G.n[0] * G.n[1] * G.n[2];
+    prof_count(KC_FWI);
     k_fold<<<(unsigned)((nint + 255) / 256), 256, 0, st>>>(op->lev[0].nx, op->lev[0].ny, op->lev[0].nz, (int)G.n[0],
                                                            (int)G.n[1], (int)G.n[2], G.pml[0][0], G.pml[1][0],
                                                            G.pml[2][0], fb.gext, fb.f, fg);
@@ -1000,6 +1089,33 @@ helm_status helm_transfer(helm_op* op, int32_t level, int32_t prolong, int32_t n
     }
   });
 }
+
+helm_status helm_profile(int32_t enable, int32_t stride) {
+  return wrap([&] {
+    REQ(stride >= 1, HELM_ERR_ARG, "stride must be >= 1");
+    prof_drain();
+    g_prof.on = enable != 0;
+    g_prof.stride = stride;
+    for (int c = 0; c < HELM_NCLASS; ++c) {
+      g_prof.launches[c] = g_prof.sampled[c] = 0;
+      g_prof.ms[c] = g_prof.bytes[c] = 0.0;
+    }
+  });
+}
+
+helm_status helm_profile_read(int64_t* launches, int64_t* sampled, double* ms, double* bytes) {
+  return wrap([&] {
+    prof_drain();
+    for (int c = 0; c < HELM_NCLASS; ++c) {
+      if (launches) launches[c] = g_prof.launches[c];
+      if (sampled) sampled[c] = g_prof.sampled[c];
+      if (ms) ms[c] = g_prof.ms[c];
+      if (bytes) bytes[c] = g_prof.bytes[c];
+    }
+  });
+}
+
+int64_t helm_launch_count(void) { return g_launches; }
 
 double helm_workspace_vectors(const helm_op* op) { return op ? op->ws_vectors : 0.0; }
 
