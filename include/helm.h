@@ -62,7 +62,8 @@ typedef struct {
  * fwi_* require v_ref > 0 so that H depends on m only through omega^2 diag(E m) (Eq. 7). */
 typedef struct { double R; int32_t power; double v_ref; } helm_pml;
 
-/* §5: memory vector (k_so, k_si, k_co, k_ci) = (3,5,3,5), levels = 3 grids (R20). */
+/* §5: memory vector (k_so, k_si, k_co, k_ci) = (3,5,3,5), levels = 3 grids (R20).
+ * levels = 0 builds an operator-only op (helm_apply only; no hierarchy or Krylov workspace). */
 typedef struct { int32_t levels, ks_o, ks_i, kc_o, kc_i; } helm_mlopts;
 
 /* outer FGMRES(k_inner) restarted until the TRUE ||b - Hx||/||b|| <= rtol per RHS
@@ -161,10 +162,12 @@ helm_status helm_transfer(helm_op* op, int32_t level, int32_t prolong, int32_t n
  * recorded on the stream it is launched on. Resets the accumulated statistics. */
 helm_status helm_profile(int32_t enable, int32_t stride);
 
-/* Per class (arrays of HELM_NCLASS): launches since the last helm_profile call, sampled
- * launches, summed device ms of the sampled launches, summed algorithmic bytes of the
- * sampled launches. Synchronizes on the recorded events. */
-helm_status helm_profile_read(int64_t* launches, int64_t* sampled, double* ms, double* bytes);
+/* Per class (arrays of HELM_NCLASS) for grid level `level` (0 = finest .. 3; 4 = kernels
+ * without a level; -1 = all): launches since the last helm_profile call, sampled launches,
+ * summed device ms of the sampled launches, summed algorithmic bytes of the sampled
+ * launches. Synchronizes on the recorded events. */
+helm_status helm_profile_read(int32_t level, int64_t* launches, int64_t* sampled, double* ms,
+                              double* bytes);
 
 /* Total kernel launches issued by this library since it was loaded. */
 int64_t     helm_launch_count(void);

@@ -65,7 +65,7 @@ SIGNATURES = {
     "helm_transfer": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),
     "helm_workspace_vectors": (C.c_double, [_P]),
     "helm_profile": (C.c_int, [C.c_int32, C.c_int32]),
-    "helm_profile_read": (C.c_int, [_i64, _i64, _d, _d]),
+    "helm_profile_read": (C.c_int, [C.c_int32, _i64, _i64, _d, _d]),
     "helm_launch_count": (C.c_int64, []),
     "helm_destroy": (None, [_P]),
     "helm_last_error": (C.c_char_p, []),

@@ -249,14 +249,14 @@ def profile(enable: bool, stride: int = 1):
     L.check(L.load().helm_profile(int(enable), int(stride)))
 
 
-def profile_read() -> dict:
+def profile_read(level: int = -1) -> dict:
     lib = L.load()
     n = L.NCLASS
     la = np.zeros(n, np.int64)
     sa = np.zeros(n, np.int64)
     ms = np.zeros(n)
     by = np.zeros(n)
-    L.check(lib.helm_profile_read(_i64ptr(la), _i64ptr(sa), _dptr(ms), _dptr(by)))
+    L.check(lib.helm_profile_read(level, _i64ptr(la), _i64ptr(sa), _dptr(ms), _dptr(by)))
     return {L.CLASS_NAMES[c]: {"launches": int(la[c]), "sampled": int(sa[c]), "ms": float(ms[c]),
                                "bytes": float(by[c])} for c in range(n)}
 

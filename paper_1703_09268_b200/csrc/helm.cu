@@ -2,7 +2,7 @@
 // level hierarchy, Krylov workspace), the FGMRES / ML-GMRES orchestration and the C ABI
 // declared in include/helm.h. All numerics run in the kernels of kernels.cuh.
 #include "helm.h"
-#include "kernels.cuh"
+#include "stencil.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -10,6 +10,7 @@
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -40,14 +41,15 @@ constexpr int K1 = HELM_KMAX + 1;
 // ------------------------------------------------------------------------------ probes
 enum KClass { KC_STENCIL = 0, KC_RESID, KC_NORM, KC_DOTS, KC_UPDATE, KC_SOLUPD, KC_COPY, KC_RESTRICT,
               KC_PROLONG, KC_FWI, KC_SETUP };
-struct ProbeRec { int cls; cudaEvent_t a, b; double bytes; };
+struct ProbeRec { int cls, level; cudaEvent_t a, b; double bytes; };
 struct Prof {
   bool on = false;
   int stride = 1;
-  long long launches[HELM_NCLASS] = {};
-  long long sampled[HELM_NCLASS] = {};
-  double ms[HELM_NCLASS] = {};
-  double bytes[HELM_NCLASS] = {};
+  long long launches[HELM_NCLASS][5] = {};   // [class][level 0..3, 4 = no level]
+  long long sampled[HELM_NCLASS][5] = {};
+  double ms[HELM_NCLASS][5] = {};
+  double bytes[HELM_NCLASS][5] = {};
+  int cur_level = 4;
   std::vector<ProbeRec> pending;
   std::vector<cudaEvent_t> pool;
   cudaEvent_t cur_a = nullptr;
@@ -69,13 +71,14 @@ cudaEvent_t prof_event() {
 // Launch counted but never timed (setup / FWI bookkeeping kernels).
 inline void prof_count(int cls) {
   ++g_launches;
-  if (g_prof.on) g_prof.launches[cls]++;
+  if (g_prof.on) g_prof.launches[cls][4]++;
 }
 // Call immediately before a launch on stream st.
-inline void prof_begin(int cls, cudaStream_t st) {
+inline void prof_begin(int cls, cudaStream_t st, int level) {
   ++g_launches;
   if (!g_prof.on) return;
-  g_prof.cur_sampled = (g_prof.launches[cls]++ % g_prof.stride) == 0;
+  g_prof.cur_level = level;
+  g_prof.cur_sampled = (g_prof.launches[cls][level]++ % g_prof.stride) == 0;
   if (g_prof.cur_sampled) {
     g_prof.cur_a = prof_event();
     cudaEventRecord(g_prof.cur_a, st);
@@ -86,7 +89,7 @@ inline void prof_end(int cls, cudaStream_t st, double bytes) {
   if (!g_prof.on || !g_prof.cur_sampled) return;
   cudaEvent_t b = prof_event();
   cudaEventRecord(b, st);
-  g_prof.pending.push_back({cls, g_prof.cur_a, b, bytes});
+  g_prof.pending.push_back({cls, g_prof.cur_level, g_prof.cur_a, b, bytes});
   g_prof.cur_sampled = false;
 }
 void prof_drain() {
@@ -94,9 +97,9 @@ void prof_drain() {
     cudaEventSynchronize(r.b);
     float t = 0.f;
     cudaEventElapsedTime(&t, r.a, r.b);
-    g_prof.ms[r.cls] += t;
-    g_prof.bytes[r.cls] += r.bytes;
-    g_prof.sampled[r.cls] += 1;
+    g_prof.ms[r.cls][r.level] += t;
+    g_prof.bytes[r.cls][r.level] += r.bytes;
+    g_prof.sampled[r.cls][r.level] += 1;
     g_prof.pool.push_back(r.a);
     g_prof.pool.push_back(r.b);
   }
@@ -174,6 +177,7 @@ struct helm_op {
   std::vector<double> bytes;
   std::vector<int64_t> mv[4];
   double ws_vectors = 0.0;
+  bool apply_only = false;
   ~helm_op() {
     for (void* p : allocs) cudaFree(p);
   }
@@ -233,37 +237,87 @@ template <> Geo<float> geo<float>(const helm_op* op, int l, int adj) {
 }
 
 // ------------------------------------------------------------------------------ launchers
+template <int N = 1, typename F> void dispatch_k(int k, F&& f) {
+  if constexpr (N <= HELM_KMAX) {
+    if (k == N) { f(std::integral_constant<int, N>{}); return; }
+    dispatch_k<N + 1>(k, f);
+  } else {
+    throw HelmErr{HELM_ERR_ARG, "Krylov dimension out of range"};
+  }
+}
+
+template <typename R, int MODE, int NV> constexpr int plane_stages() {
+  constexpr int NP = MODE == 1 ? 1 : (MODE == 2 ? NV : 0);
+  constexpr size_t sb = PlaneSmem<R, 32, 8, NP>::stage_bytes;
+  constexpr int st = (int)((56 * 1024) / sb);
+  return st < 4 ? 4 : (st > 8 ? 8 : st);
+}
+
+template <typename R, int MODE, int NV, bool YC>
+void run_plane(const PlaneArgs<R>& a, dim3 grid, cudaStream_t st) {
+  constexpr int S = plane_stages<R, MODE, NV>();
+  constexpr int NP = MODE == 1 ? 1 : (MODE == 2 ? NV : 0);
+  constexpr int PY = YC ? 2 : 1;
+  const size_t smem = S * PlaneSmem<R, 32, 8, NP>::stage_bytes;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_plane<R, 32, 8, PY, S, MODE, NV, YC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    attr = true;
+  }
+  k_plane<R, 32, 8, PY, S, MODE, NV, YC><<<grid, 32 * 8 / PY, smem, st>>>(a);
+}
+
+// z-chunking shared by the launcher and the reduction-scratch sizing
+inline int plane_nzc(long long ctas_per_z, int nz) {
+  const long long target = 148LL * 8;
+  long long nzc = (target + ctas_per_z - 1) / ctas_per_z;
+  nzc = std::max(1LL, std::min(nzc, (long long)std::max(1, nz / 4)));
+  nzc = std::max(nzc, (long long)((nz + 63) / 64));
+  return (int)nzc;
+}
+
+// Plane-streaming stencil (stencil.cuh). mode 0: y = s H x; 1: y = b - H x (+cycle start);
+// 2: y = s H x with the fused projections h_ij = <V_i, y>, i < nv (nv = j + 1).
+// 3D: 32x8 (x,y) tiles, one RHS per CTA; 2D: 32 x-points x 8 right-hand sides per CTA.
+template <typename R>
+void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* x, cx<R>* y, const cx<R>* b,
+                  const VPtrs<R>* V, int nv, const double* xscale, const int* kact, int j, const KCtx& ctx) {
+  PlaneArgs<R> a{};
+  a.g = geo<R>(op, l, adj);
+  a.x = x; a.y = y; a.b = b;
+  if (V) a.V = *V;
+  a.xscale = xscale; a.sstride = K1; a.active = op->active_d; a.kact = kact; a.jstep = j;
+  a.nrhs = nrhs; a.ctx = ctx; a.rb = op->rb;
+  const bool d3 = a.g.ny > 1;
+  a.ntx = (a.g.nx + 31) / 32;
+  a.nty = d3 ? (a.g.ny + 7) / 8 : (nrhs + 7) / 8;
+  const long long ctas_per_z = (long long)a.ntx * a.nty * (d3 ? nrhs : 1);
+  const int nzc0 = plane_nzc(ctas_per_z, a.g.nz);
+  a.zlen = (a.g.nz + nzc0 - 1) / nzc0;
+  const int nzc = (a.g.nz + a.zlen - 1) / a.zlen;
+  const dim3 grid((unsigned)ctas_per_z, (unsigned)nzc);
+  const int cls = mode == 0 ? KC_STENCIL : (mode == 1 ? KC_RESID : KC_DOTS);
+  prof_begin(cls, op->st, l);
+  if (d3) {
+    if (mode == 0) run_plane<R, 0, 0, true>(a, grid, op->st);
+    else if (mode == 1) run_plane<R, 1, 0, true>(a, grid, op->st);
+    else dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, true>(a, grid, op->st); });
+  } else {
+    if (mode == 0) run_plane<R, 0, 0, false>(a, grid, op->st);
+    else if (mode == 1) run_plane<R, 1, 0, false>(a, grid, op->st);
+    else dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, false>(a, grid, op->st); });
+  }
+  CKL();
+  const double Sc = sizeof(cx<R>), Sr = sizeof(R);
+  const double per = mode == 0 ? 2 * Sc + Sr : (mode == 1 ? 3 * Sc + Sr : (2 + nv) * Sc + Sr);
+  prof_end(cls, op->st, acct(op, l, per * a.g.N, true, nrhs));
+}
+
 template <typename R>
 void launch_stencil(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* x, cx<R>* y,
                     const cx<R>* b, const double* xscale, const int* kact, int j, const KCtx& ctx) {
-  const Geo<R> g = geo<R>(op, l, adj);
-  const bool d3 = g.ny > 1;
-  const int BX = d3 ? 32 : 64, BY = d3 ? 8 : 1;
-  const int ntx = (g.nx + BX - 1) / BX, nty = (g.ny + BY - 1) / BY;
-  const long long tiles = (long long)ntx * nty;
-  const int thr_per_blk = BX * BY;
-  long long target = (long long)TARGET_BLOCKS * 256 / thr_per_blk;
-  long long nzc = std::max(1LL, std::min((target + tiles * nrhs - 1) / (tiles * nrhs), (long long)std::max(1, g.nz / 8)));
-  int zlen = (int)((g.nz + nzc - 1) / nzc);
-  nzc = (g.nz + zlen - 1) / zlen;
-  dim3 grid((unsigned)(tiles * nrhs), (unsigned)nzc);
-  const int* act = op->active_d;
-  const size_t S = sizeof(cx<R>);
-  const int cls = mode ? KC_RESID : KC_STENCIL;
-  prof_begin(cls, op->st);
-  if (d3) {
-    if (mode == 0)
-      k_stencil<R, 32, 8, 0><<<grid, 256, 0, op->st>>>(g, x, y, b, xscale, K1, act, kact, j, nrhs, ntx, nty, zlen, ctx, op->rb);
-    else
-      k_stencil<R, 32, 8, 1><<<grid, 256, 0, op->st>>>(g, x, y, b, xscale, K1, act, kact, j, nrhs, ntx, nty, zlen, ctx, op->rb);
-  } else {
-    if (mode == 0)
-      k_stencil<R, 64, 1, 0><<<grid, 64, 0, op->st>>>(g, x, y, b, xscale, K1, act, kact, j, nrhs, ntx, nty, zlen, ctx, op->rb);
-    else
-      k_stencil<R, 64, 1, 1><<<grid, 64, 0, op->st>>>(g, x, y, b, xscale, K1, act, kact, j, nrhs, ntx, nty, zlen, ctx, op->rb);
-  }
-  CKL();
-  prof_end(cls, op->st, acct(op, l, (mode == 0 ? 2.0 : 3.0) * S * g.N + sizeof(R) * g.N, true, nrhs));
+  launch_plane<R>(op, l, adj, mode, nrhs, x, y, b, nullptr, 0, xscale, kact, j, ctx);
 }
 
 template <typename R> VPtrs<R> vptrs(cx<R>* const* V, const cx<R>* v0, int n) {
@@ -276,28 +330,20 @@ template <typename R>
 void launch_norm_start(helm_op* op, int l, int nrhs, const cx<R>* b, const KCtx& ctx) {
   const long long N = op->lev[l].N;
   dim3 grid(blas_blocks(N, nrhs), nrhs);
-  prof_begin(KC_NORM, op->st);
+  prof_begin(KC_NORM, op->st, l);
   k_norm_start<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, b, op->active_d, ctx, op->rb);
   CKL();
   prof_end(KC_NORM, op->st, acct(op, l, sizeof(cx<R>) * (double)N, false, nrhs));
 }
 
 template <typename R>
-void launch_dots(helm_op* op, int l, int nrhs, const VPtrs<R>& V, int j, const cx<R>* w, const KCtx& ctx) {
-  const long long N = op->lev[l].N;
-  dim3 grid(blas_blocks(N, nrhs), nrhs);
-  prof_begin(KC_DOTS, op->st);
-  k_dots<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, V, j, w, op->active_d, ctx, op->rb);
-  CKL();
-  prof_end(KC_DOTS, op->st, acct(op, l, (j + 2.0) * sizeof(cx<R>) * N, false, nrhs));
-}
-
-template <typename R>
 void launch_update(helm_op* op, int l, int nrhs, const VPtrs<R>& V, int j, cx<R>* w, const KCtx& ctx) {
   const long long N = op->lev[l].N;
   dim3 grid(blas_blocks(N, nrhs), nrhs);
-  prof_begin(KC_UPDATE, op->st);
-  k_update<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, V, j, w, op->active_d, ctx, op->rb);
+  prof_begin(KC_UPDATE, op->st, l);
+  dispatch_k(j + 1, [&](auto c) {
+    k_update_t<R, decltype(c)::value><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, V, j, w, op->active_d, ctx, op->rb);
+  });
   CKL();
   prof_end(KC_UPDATE, op->st, acct(op, l, (j + 3.0) * sizeof(cx<R>) * N, false, nrhs));
 }
@@ -307,8 +353,10 @@ void launch_solupdate(helm_op* op, int l, int nrhs, const VPtrs<R>& Z, const dou
                       int init, int k, const KCtx& ctx) {
   const long long N = op->lev[l].N;
   dim3 grid(blas_blocks(N, nrhs), nrhs);
-  prof_begin(KC_SOLUPD, op->st);
-  k_solupdate<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, Z, zscale, x, init, op->active_d, ctx);
+  prof_begin(KC_SOLUPD, op->st, l);
+  dispatch_k(k, [&](auto c) {
+    k_solupdate_t<R, decltype(c)::value><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, Z, zscale, x, init, op->active_d, ctx);
+  });
   CKL();
   prof_end(KC_SOLUPD, op->st, acct(op, l, (k + (init ? 1.0 : 2.0)) * sizeof(cx<R>) * N, false, nrhs));
 }
@@ -318,7 +366,7 @@ void launch_copy_scale(helm_op* op, int l, int nrhs, const Ti* in, To* out, cons
                        const int* kact, int j) {
   const long long N = op->lev[l].N;
   dim3 grid(blas_blocks(N, nrhs), nrhs);
-  prof_begin(KC_COPY, op->st);
+  prof_begin(KC_COPY, op->st, l);
   k_copy_scale<Ti, To><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, in, out, scale, K1, kact, j, op->active_d);
   CKL();
   prof_end(KC_COPY, op->st, acct(op, l, (double)(sizeof(Ti) + sizeof(To)) * N, false, nrhs));
@@ -329,7 +377,7 @@ void launch_restrict(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* out) 
   const LevelDev &F = op->lev[l], &Cc = op->lev[l + 1];
   dim3 grid(blas_blocks(Cc.N, nrhs), nrhs);
   const R fac = (R)std::ldexp(1.0, -op->dim);
-  prof_begin(KC_RESTRICT, op->st);
+  prof_begin(KC_RESTRICT, op->st, l);
   k_restrict<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3, fac,
                                                        in, out, op->active_d);
   CKL();
@@ -340,7 +388,7 @@ template <typename R>
 void launch_prolong_add(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* out) {
   const LevelDev &F = op->lev[l], &Cc = op->lev[l + 1];
   dim3 grid(blas_blocks(F.N, nrhs), nrhs);
-  prof_begin(KC_PROLONG, op->st);
+  prof_begin(KC_PROLONG, op->st, l);
   k_prolong_add<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3,
                                                           in, out, op->active_d);
   CKL();
@@ -379,8 +427,7 @@ void krylov(helm_op* op, int l, int adj, int nrhs, KCtx& ctx, int ko, int ki, bo
         zj = Vp.p[j];
         zs = ctx.scale + j;
       }
-      launch_stencil<R>(op, l, adj, 0, nrhs, zj, V[j + 1], nullptr, zs, ctx.kact, j, ctx);
-      launch_dots<R>(op, l, nrhs, Vp, j, V[j + 1], ctx);
+      launch_plane<R>(op, l, adj, 2, nrhs, zj, V[j + 1], nullptr, &Vp, j + 1, zs, ctx.kact, j, ctx);
       launch_update<R>(op, l, nrhs, Vp, j, V[j + 1], ctx);
     }
     if (flex) {
@@ -548,7 +595,9 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
   REQ(dtype == HELM_C64 || dtype == HELM_C128, HELM_ERR_ARG, "bad dtype");
   REQ(max_rhs >= 1, HELM_ERR_ARG, "max_rhs must be >= 1");
   helm_mlopts o = mlo ? *mlo : helm_mlopts{3, 3, 5, 3, 5};
-  REQ(o.levels >= 1 && o.levels <= 4, HELM_ERR_ARG, "levels must be in [1,4]");
+  const bool apply_only = o.levels == 0;   // operator-only op: helm_apply, no solver workspace
+  if (apply_only) o.levels = 1;
+  REQ(o.levels >= 1 && o.levels <= 4, HELM_ERR_ARG, "levels must be in [0,4]");
   REQ(o.ks_o >= 1 && o.ks_i >= 1 && o.kc_o >= 1 && o.kc_i >= 1, HELM_ERR_ARG, "Krylov counts must be >= 1");
   REQ(o.ks_i <= HELM_KMAX && o.kc_i <= HELM_KMAX && k_inner <= HELM_KMAX && k_inner >= 1, HELM_ERR_ARG,
       "inner Krylov dimension exceeds HELM_KMAX");
@@ -605,15 +654,25 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
   for (int l = 0; l < L; ++l) {
     const LevelDev& Lv = op->lev[l];
     const bool d3 = Lv.ny > 1;
-    const int BX = d3 ? 32 : 64, BY = d3 ? 8 : 1;
-    long long tiles = (long long)((Lv.nx + BX - 1) / BX) * ((Lv.ny + BY - 1) / BY);
-    pst = std::max(pst, tiles * std::max(1, Lv.nz / 8 + 1));
+    const long long ntx = (Lv.nx + 31) / 32, nty = d3 ? (Lv.ny + 7) / 8 : 1;
+    const long long nzc_max = std::max(1, Lv.nz / 4) + (Lv.nz + 63) / 64 + 1;
+    pst = std::max(pst, (long long)K1 * ntx * nty * nzc_max * (d3 ? 4 : 1));
   }
   op->rb.pstride = pst;
   op->rb.part = dalloc<double2>(op->allocs, (size_t)pst * max_rhs);
   op->rb.ticket = dalloc<unsigned>(op->allocs, max_rhs);
   CK(cudaMemset(op->rb.ticket, 0, sizeof(unsigned) * max_rhs));
   op->active_d = dalloc<int>(op->allocs, max_rhs);
+  op->apply_only = apply_only;
+  if (apply_only) {
+    op->act_h.assign(max_rhs, 1);
+    op->bytes.assign(max_rhs, 0.0);
+    for (int l = 0; l < 4; ++l) op->mv[l].assign(max_rhs, 0);
+    op_set_model(op.get(), m);
+    op_set_omega(op.get(), omega);
+    CK(cudaStreamSynchronize(st));
+    return op.release();
+  }
   // outer FGMRES (always complex128, D15) + V-cycle workspace in the V-cycle precision
   const size_t n0 = (size_t)op->lev[0].N * max_rhs;
   for (int i = 0; i <= k_inner; ++i) op->OV[i] = dalloc<double2>(op->allocs, n0);
@@ -713,8 +772,7 @@ void solve_c128(helm_op* op, int adj, int nrhs, const double2* B, double2* X, co
         zj = Vp.p[j];
         zs = ctx.scale + j;
       }
-      launch_stencil<double>(op, 0, adj, 0, nrhs, zj, op->OV[j + 1], nullptr, zs, ctx.kact, j, ctx);
-      launch_dots<double>(op, 0, nrhs, Vp, j, op->OV[j + 1], ctx);
+      launch_plane<double>(op, 0, adj, 2, nrhs, zj, op->OV[j + 1], nullptr, &Vp, j + 1, zs, ctx.kact, j, ctx);
       launch_update<double>(op, 0, nrhs, Vp, j, op->OV[j + 1], ctx);
     }
     if (precond) {
@@ -963,6 +1021,7 @@ helm_status helm_solve(helm_op* op, int32_t adjoint, int32_t nrhs, const void* b
     REQ(nrhs >= 1 && nrhs <= op->max_rhs, HELM_ERR_SHAPE, "nrhs must be in [1, max_rhs]");
     REQ(adjoint == 0 || adjoint == 1, HELM_ERR_ARG, "adjoint must be 0 or 1");
     REQ(b != x, HELM_ERR_ARG, "b and x must not alias");
+    REQ(!op->apply_only, HELM_ERR_STATE, "operator-only op (mlopts.levels = 0) cannot solve");
     helm_solve_opts so = opts ? *opts : default_solve_opts(op);
     check_solve_opts(op, so);
     op->st = (cudaStream_t)stream;
@@ -1053,6 +1112,7 @@ helm_status helm_get_level(const helm_op* op, int32_t level, int32_t adjoint, in
 helm_status helm_vcycle(helm_op* op, int32_t level, int32_t adjoint, int32_t nrhs, const void* b, void* z, void* stream) {
   return wrap([&] {
     level_ptr_check(op, level);
+    REQ(!op->apply_only, HELM_ERR_STATE, "operator-only op");
     REQ(level < op->L - 1, HELM_ERR_ARG, "no V-cycle on the coarsest level");
     REQ(b && z && b != z, HELM_ERR_ARG, "bad vectors");
     REQ(nrhs >= 1 && nrhs <= op->max_rhs, HELM_ERR_SHAPE, "nrhs must be in [1, max_rhs]");
@@ -1096,21 +1156,29 @@ helm_status helm_profile(int32_t enable, int32_t stride) {
     prof_drain();
     g_prof.on = enable != 0;
     g_prof.stride = stride;
-    for (int c = 0; c < HELM_NCLASS; ++c) {
-      g_prof.launches[c] = g_prof.sampled[c] = 0;
-      g_prof.ms[c] = g_prof.bytes[c] = 0.0;
-    }
+    for (int c = 0; c < HELM_NCLASS; ++c)
+      for (int l = 0; l < 5; ++l) {
+        g_prof.launches[c][l] = g_prof.sampled[c][l] = 0;
+        g_prof.ms[c][l] = g_prof.bytes[c][l] = 0.0;
+      }
   });
 }
 
-helm_status helm_profile_read(int64_t* launches, int64_t* sampled, double* ms, double* bytes) {
+helm_status helm_profile_read(int32_t level, int64_t* launches, int64_t* sampled, double* ms, double* bytes) {
   return wrap([&] {
+    REQ(level >= -1 && level <= 4, HELM_ERR_ARG, "level must be in [-1, 4]");
     prof_drain();
     for (int c = 0; c < HELM_NCLASS; ++c) {
-      if (launches) launches[c] = g_prof.launches[c];
-      if (sampled) sampled[c] = g_prof.sampled[c];
-      if (ms) ms[c] = g_prof.ms[c];
-      if (bytes) bytes[c] = g_prof.bytes[c];
+      long long la = 0, sa = 0;
+      double m = 0, b = 0;
+      for (int l = 0; l < 5; ++l)
+        if (level < 0 || l == level) {
+          la += g_prof.launches[c][l]; sa += g_prof.sampled[c][l]; m += g_prof.ms[c][l]; b += g_prof.bytes[c][l];
+        }
+      if (launches) launches[c] = la;
+      if (sampled) sampled[c] = sa;
+      if (ms) ms[c] = m;
+      if (bytes) bytes[c] = b;
     }
   });
 }

@@ -571,3 +571,148 @@ __global__ void k_fold(int Nx, int Ny, int Nz, int nx, int ny, int nz, int wx, i
       for (int i = xa; i <= xb; ++i) s += gext[((long long)k * Ny + j) * Nx + i];
   fg[1 + p] = s;
 }
+
+// ================================================================= a3/a4 BLAS-1, templated
+// NV = j+1 basis vectors known at compile time; 2 points per thread per iteration so every
+// thread has 2*(NV+1) independent 16-byte loads in flight.
+template <typename R, int NV>
+__global__ void __launch_bounds__(HELM_RED_THREADS)
+k_update_t(long long N, VPtrs<R> V, int j, cx<R>* __restrict__ w, const int* __restrict__ active, KCtx ctx,
+           RedBuf rb) {
+  const int r = blockIdx.y;
+  if (active && !active[r]) return;
+  if (j >= ctx.kact[r]) return;
+  const long long off = (long long)r * N;
+  cx<R>* wr = w + off;
+  cx<R> coef[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const double2 h = ctx.H[(long long)r * (HELM_KMAX + 1) * HELM_KMAX + hidx(i, j)];
+    const double sc = ctx.scale[r * (HELM_KMAX + 1) + i];
+    coef[i] = from_d<cx<R>>(make_double2(-h.x * sc, -h.y * sc));
+  }
+  const cx<R>* vp[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) vp[i] = V.p[i] + off;
+  double s = 0.0;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; p + gs < N; p += 2 * gs) {
+    cx<R> w0 = wr[p], w1 = wr[p + gs];
+    cx<R> a0[NV], a1[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) { a0[i] = vp[i][p]; a1[i] = vp[i][p + gs]; }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) { w0 = cfma(coef[i], a0[i], w0); w1 = cfma(coef[i], a1[i], w1); }
+    wr[p] = w0;
+    wr[p + gs] = w1;
+    s += (double)w0.x * w0.x + (double)w0.y * w0.y + (double)w1.x * w1.x + (double)w1.y * w1.y;
+  }
+  if (p < N) {
+    cx<R> w0 = wr[p];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) w0 = cfma(coef[i], vp[i][p], w0);
+    wr[p] = w0;
+    s += (double)w0.x * w0.x + (double)w0.y * w0.y;
+  }
+  __shared__ double2 sm[32];
+  __shared__ double2 tot[1];
+  double2 v[1] = {make_double2(s, 0.0)};
+  if (grid_sum_last<1>(v, 1, rb.part + r * rb.pstride, rb.ticket + r, blockIdx.x, gridDim.x, sm, tot)) {
+    if (threadIdx.x == 0) {
+      const int K1 = HELM_KMAX + 1;
+      double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
+      double* cs = ctx.cs + r * HELM_KMAX;
+      double2* sn = ctx.sn + r * HELM_KMAX;
+      double2* gv = ctx.g + r * K1;
+      const double hn = sqrt(tot[0].x);
+      for (int i = 0; i < j; ++i) {   // previous rotations on column j
+        const double2 a = H[hidx(i, j)], bb = H[hidx(i + 1, j)];
+        const double c = cs[i];
+        const double2 sv = sn[i];
+        H[hidx(i, j)] = cadd(make_double2(c * a.x, c * a.y), cmul(sv, bb));
+        H[hidx(i + 1, j)] = csub(make_double2(c * bb.x, c * bb.y), cmul(cconj(sv), a));
+      }
+      const double2 a = H[hidx(j, j)];
+      const double aa = sqrt(cabs2(a)), rr = sqrt(aa * aa + hn * hn);
+      double c;
+      double2 sv;
+      if (rr == 0.0) { c = 1.0; sv = make_double2(0.0, 0.0); }
+      else if (aa == 0.0) { c = 0.0; sv = make_double2(1.0, 0.0); }
+      else { c = aa / rr; sv = make_double2(a.x / aa * hn / rr, a.y / aa * hn / rr); }
+      cs[j] = c; sn[j] = sv;
+      H[hidx(j, j)] = cadd(make_double2(c * a.x, c * a.y), make_double2(sv.x * hn, sv.y * hn));
+      H[hidx(j + 1, j)] = make_double2(0.0, 0.0);
+      const double2 gj = gv[j];
+      gv[j + 1] = cmul(make_double2(-sv.x, sv.y), gj);   // -conj(s) g_j
+      gv[j] = make_double2(c * gj.x, c * gj.y);
+      if (hn <= 1e-14 * ctx.beta[r]) {                    // breakdown guard (D14)
+        ctx.kact[r] = j + 1;
+        ctx.scale[r * K1 + j + 1] = 0.0;
+      } else {
+        ctx.scale[r * K1 + j + 1] = 1.0 / hn;
+      }
+    }
+  }
+}
+
+// x <- (init ? 0 : x) + sum_{i<kact} y_i z_i, R y = g by back substitution (per block).
+template <typename R, int K>
+__global__ void __launch_bounds__(HELM_RED_THREADS)
+k_solupdate_t(long long N, VPtrs<R> Z, const double* __restrict__ zscale, cx<R>* __restrict__ x, int init,
+              const int* __restrict__ active, KCtx ctx) {
+  const int r = blockIdx.y;
+  if (active && !active[r]) return;
+  __shared__ cx<R> yc[K];
+  __shared__ int s_k;
+  if (threadIdx.x == 0) {
+    const int K1 = HELM_KMAX + 1;
+    const int k = ctx.kact[r];
+    const double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
+    const double2* gv = ctx.g + r * K1;
+    double2 yv[K];
+    for (int i = K - 1; i >= 0; --i) {
+      if (i >= k) { yv[i] = make_double2(0.0, 0.0); continue; }
+      double2 t = gv[i];
+      for (int l = i + 1; l < k; ++l) t = csub(t, cmul(H[hidx(i, l)], yv[l]));
+      const double2 d = H[hidx(i, i)];
+      yv[i] = (d.x == 0.0 && d.y == 0.0) ? make_double2(0.0, 0.0) : cdiv(t, d);
+    }
+    for (int i = 0; i < K; ++i) {
+      const double sc = (zscale && i < k) ? zscale[r * K1 + i] : 1.0;
+      yc[i] = from_d<cx<R>>(make_double2(yv[i].x * sc, yv[i].y * sc));
+    }
+    s_k = k;
+  }
+  __syncthreads();
+  const int k = s_k;
+  if (k == 0 && !init) return;
+  const long long off = (long long)r * N;
+  cx<R>* xr = x + off;
+  cx<R> yl[K];
+  const cx<R>* zp[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) { yl[i] = yc[i]; zp[i] = Z.p[i] + off; }
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; p + gs < N; p += 2 * gs) {
+    cx<R> x0 = init ? mkc((R)0, (R)0) : xr[p];
+    cx<R> x1 = init ? mkc((R)0, (R)0) : xr[p + gs];
+    cx<R> a0[K], a1[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (i < k) { a0[i] = zp[i][p]; a1[i] = zp[i][p + gs]; }
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (i < k) { x0 = cfma(yl[i], a0[i], x0); x1 = cfma(yl[i], a1[i], x1); }
+    xr[p] = x0;
+    xr[p + gs] = x1;
+  }
+  if (p < N) {
+    cx<R> x0 = init ? mkc((R)0, (R)0) : xr[p];
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (i < k) x0 = cfma(yl[i], zp[i][p], x0);
+    xr[p] = x0;
+  }
+}

@@ -1,0 +1,58 @@
+"""Per-level, per-kernel-class device time of one cfg2 FWI evaluation (diagnostic).
+
+    python scripts/profile_levels.py [--dtype c128|c64] [--freq 5] [--nsrc 50]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_1703_09268_b200 import api  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--dtype", default="c128")
+    ap.add_argument("--freq", type=float, default=5.0)
+    ap.add_argument("--nsrc", type=int, default=50)
+    ap.add_argument("--stride", type=int, default=1)
+    a = ap.parse_args()
+    p = synth.cfg2(nsrc=a.nsrc, freqs=(a.freq,))
+    grid = api.Grid.of(p)
+    pml = api.Pml(v_ref=3000.0)
+    dt = api.C64 if a.dtype == "c64" else api.C128
+    d, _ = api.fwi_forward(grid, p.m_true, p.freqs, p.src, p.rec, pml, api.C128, api.SolveOpts(rtol=1e-8), max_rhs=a.nsrc)
+    api.fwi_misfit_grad(grid, p.m, p.freqs, p.src, p.rec, d, pml, dt, max_rhs=a.nsrc)   # warm
+    torch.cuda.synchronize()
+    api.profile(True, a.stride)
+    t0 = time.perf_counter()
+    fg, rep = api.fwi_misfit_grad(grid, p.m, p.freqs, p.src, p.rec, d, pml, dt, max_rhs=a.nsrc)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    out = {"wall_s": wall, "cycles": sorted({r["outer_cycles"] for r in rep}), "levels": {}}
+    tot = 0.0
+    for lvl in range(5):
+        pr = api.profile_read(lvl)
+        row = {}
+        for k, v in pr.items():
+            if v["launches"]:
+                est = v["ms"] * v["launches"] / max(v["sampled"], 1)
+                tot += est
+                row[k] = {"launches": v["launches"], "est_ms": round(est, 2),
+                          "avg_us": round(1e3 * v["ms"] / max(v["sampled"], 1), 2),
+                          "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)}
+        if row:
+            out["levels"][lvl] = row
+    out["gpu_est_s"] = tot / 1e3
+    api.profile(False, 1)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
