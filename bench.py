@@ -193,6 +193,10 @@ def run_ours(args, rank, size, dev):
     kernel_shares = {k: round(v / total_est, 3) for k, v in sorted(est.items(), key=lambda kv: -kv[1])}
 
     cycles = [r["outer_cycles"] for r in (reps or [])]
+    # whole-step algorithmic HBM bytes counted by the library (every executed kernel, SURVEY d.2)
+    step_bytes = sum(r["bytes_alg"] for r in (reps or []))
+    solve_roof = {"alg_bytes_per_step": step_bytes, "achieved_GBps": round(step_bytes / (ms / args.steps / 1e3) / 1e9, 1),
+                  "frac": round(step_bytes / (ms / args.steps / 1e3) / 1e9 / peaks()[0], 4)}
     h2d = 8 * grid.n_interior + 16 * d_obs.size + 8 * (nsrc + len(prob.rec)) + 16 * len(prob.freqs)
     d2h = 8 * (1 + grid.n_interior)
     out = {
@@ -211,6 +215,7 @@ def run_ours(args, rank, size, dev):
         "gpu_launches": int(launches),
         "roofline": roof,
         "kernel_shares": kernel_shares,
+        "solve_roofline": solve_roof,
         "clocks": clk.summary(),
     }
     return out, prob

@@ -154,8 +154,9 @@ helm_status helm_transfer(helm_op* op, int32_t level, int32_t prolong, int32_t n
 /* ---- measurement probes (bench.py) ---------------------------------------------------- */
 
 /* Kernel classes: 0 stencil (y = H x), 1 stencil-residual (r = b - H x, ||r||), 2 norm,
- * 3 dots (CGS projections), 4 update (+norm, Givens), 5 solution update, 6 copy/convert,
- * 7 restrict, 8 prolong-add, 9 fwi (inject/gather/gradient/fold), 10 setup. */
+ * 3 arnoldi (stencil + CGS projections; the fused GMRES step), 4 update (+norm, Givens),
+ * 5 solution update, 6 copy/convert, 7 restrict, 8 prolong-add, 9 fwi (inject/gather/
+ * gradient/fold), 10 setup. */
 #define HELM_NCLASS 11
 
 /* When enable != 0, every `stride`-th launch of each class is bracketed by CUDA events
@@ -168,6 +169,13 @@ helm_status helm_profile(int32_t enable, int32_t stride);
  * launches. Synchronizes on the recorded events. */
 helm_status helm_profile_read(int32_t level, int64_t* launches, int64_t* sampled, double* ms,
                               double* bytes);
+
+/* Average device ms per launch of `reps` back-to-back launches of one hot-path kernel on
+ * the op's level workspace (contents overwritten): kind 0-4 = stencil modes (0 y = Hx,
+ * 1 residual, 2 stencil + CGS projections, 3 fused GMRES step, 4 its last step; nv = step),
+ * 10 = solution update (k = nv), 11 = CGS update (j = nv), 12 = norm. Tuning probe only. */
+helm_status helm_probe_kernel(helm_op* op, int32_t level, int32_t kind, int32_t nv, int32_t nrhs,
+                              int32_t reps, double* ms_per_launch, void* cuda_stream);
 
 /* Total kernel launches issued by this library since it was loaded. */
 int64_t     helm_launch_count(void);

@@ -137,6 +137,29 @@ def helmholtz_matrix(prob, omega: float, pml: PmlParams, m_int: Optional[np.ndar
     return (L + sp.diags(omega**2 * m_ext)).tocsr()
 
 
+def helmholtz_rows(prob, omega: float, pml: PmlParams, z_lo: int, z_hi: int,
+                   m_int: Optional[np.ndarray] = None) -> sp.csr_matrix:
+    """The rows of D5's H for the extended z-planes [z_lo, z_hi) (all x, y), shape
+    (rows, N_ext): the same Kronecker sum as helmholtz_matrix with the z factor restricted
+    to those planes, so large grids can be checked slab by slab without assembling H."""
+    m_int = prob.m if m_int is None else m_int
+    nx, ny, nz = prob.n
+    Nx, Ny, Nz = prob.next
+    (wxl, wxh), (wyl, wyh), (wzl, wzh) = prob.pml
+    Tx = second_difference(*tables_1d(Nx, nx, prob.h, wxl, wxh, omega, pml))
+    Tz = second_difference(*tables_1d(Nz, nz, prob.h, wzl, wzh, omega, pml))[z_lo:z_hi]
+    Ix, Iy = (sp.identity(k, format="csr", dtype=np.complex128) for k in (Nx, Ny))
+    Izr = sp.identity(Nz, format="csr", dtype=np.complex128)[z_lo:z_hi]
+    L = sp.kron(Izr, sp.kron(Iy, Tx)) + sp.kron(Tz, sp.kron(Iy, Ix))
+    if prob.ndim == 3:
+        Ty = second_difference(*tables_1d(Ny, ny, prob.h, wyl, wyh, omega, pml))
+        L = L + sp.kron(Izr, sp.kron(Ty, Ix))
+    m_slab = extend(prob, m_int)[z_lo:z_hi].ravel()
+    rows = np.arange(z_lo * Ny * Nx, z_hi * Ny * Nx)
+    D = sp.csr_matrix((omega**2 * m_slab, (np.arange(rows.size), rows)), shape=(rows.size, Nx * Ny * Nz))
+    return (L + D).tocsr()
+
+
 def helmholtz_adjoint_matrix(H: sp.spmatrix) -> sp.csr_matrix:
     """H^H as the explicit conjugate transpose (c.2 step 2) — deliberately not D6."""
     return H.conj().T.tocsr()

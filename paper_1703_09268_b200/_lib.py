@@ -40,7 +40,7 @@ class HelmSolveReport(C.Structure):
 HELM_OK, HELM_ERR_ARG, HELM_ERR_SHAPE, HELM_ERR_CUDA, HELM_ERR_OOM, HELM_ERR_STATE = 0, -1, -2, -3, -4, -5
 HELM_C64, HELM_C128 = 0, 1
 NCLASS = 11
-CLASS_NAMES = ["stencil", "stencil_resid", "norm", "dots", "update", "solupdate", "copy", "restrict",
+CLASS_NAMES = ["stencil", "stencil_resid", "norm", "arnoldi", "update", "solupdate", "copy", "restrict",
                "prolong_add", "fwi", "setup"]
 
 _P = C.c_void_p
@@ -66,6 +66,7 @@ SIGNATURES = {
     "helm_workspace_vectors": (C.c_double, [_P]),
     "helm_profile": (C.c_int, [C.c_int32, C.c_int32]),
     "helm_profile_read": (C.c_int, [C.c_int32, _i64, _i64, _d, _d]),
+    "helm_probe_kernel": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _d, _P]),
     "helm_launch_count": (C.c_int64, []),
     "helm_destroy": (None, [_P]),
     "helm_last_error": (C.c_char_p, []),

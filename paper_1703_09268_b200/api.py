@@ -261,5 +261,12 @@ def profile_read(level: int = -1) -> dict:
                                "bytes": float(by[c])} for c in range(n)}
 
 
+def probe_kernel(op: HelmOp, level: int, kind: int, nv: int, nrhs: int, reps: int = 50, stream=None) -> float:
+    """Average device ms per launch of one hot-path kernel (see helm.h helm_probe_kernel)."""
+    ms = C.c_double()
+    L.check(L.load().helm_probe_kernel(op.handle, level, kind, nv, nrhs, reps, C.byref(ms), _stream(stream)))
+    return ms.value
+
+
 def launch_count() -> int:
     return int(L.load().helm_launch_count())

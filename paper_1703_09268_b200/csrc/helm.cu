@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -136,10 +137,12 @@ struct LevelDev {
 };
 
 template <typename R> struct LevelWS {
-  cx<R>* SV[K1] = {};   // smoother basis (GMRES), SV[0] also the V-cycle residual
+  cx<R>* SV[K1] = {};   // smoother basis (GMRES), SV[0] also the V-cycle residual; SV[k] raw W
+  cx<R>* SW = nullptr;  // second raw-W buffer of the fused GMRES steps (ping-pong with SV[k])
   cx<R>* VB = nullptr;  // V-cycle input copy (scaled basis vector of the caller)
   cx<R>* VX = nullptr;  // level-0 V-cycle output in mixed mode
   cx<R>* FV[K1] = {};   // coarse-solve basis at this level
+  cx<R>* FW = nullptr;  // second raw-W buffer of the coarsest (unpreconditioned) GMRES
   cx<R>* FZ[HELM_KMAX] = {};
   cx<R>* Fx = nullptr;
   cx<R>* Fb = nullptr;
@@ -246,71 +249,103 @@ template <int N = 1, typename F> void dispatch_k(int k, F&& f) {
   }
 }
 
-template <typename R, int MODE, int NV> constexpr int plane_stages() {
-  constexpr int NP = MODE == 1 ? 1 : (MODE == 2 ? NV : 0);
-  constexpr size_t sb = PlaneSmem<R, 32, 8, NP>::stage_bytes;
-  constexpr int st = (int)((56 * 1024) / sb);
-  return st < 4 ? 4 : (st > 8 ? 8 : st);
-}
-
-template <typename R, int MODE, int NV, bool YC>
-void run_plane(const PlaneArgs<R>& a, dim3 grid, cudaStream_t st) {
-  constexpr int S = plane_stages<R, MODE, NV>();
-  constexpr int NP = MODE == 1 ? 1 : (MODE == 2 ? NV : 0);
-  constexpr int PY = YC ? 2 : 1;
-  const size_t smem = S * PlaneSmem<R, 32, 8, NP>::stage_bytes;
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_plane<R, 32, 8, PY, S, MODE, NV, YC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    attr = true;
+template <int N = 0, typename F> void dispatch_k0(int k, F&& f) {
+  if constexpr (N < HELM_KMAX) {
+    if (k == N) { f(std::integral_constant<int, N>{}); return; }
+    dispatch_k0<N + 1>(k, f);
+  } else {
+    throw HelmErr{HELM_ERR_ARG, "Krylov step out of range"};
   }
-  k_plane<R, 32, 8, PY, S, MODE, NV, YC><<<grid, 32 * 8 / PY, smem, st>>>(a);
 }
 
-// z-chunking shared by the launcher and the reduction-scratch sizing
-inline int plane_nzc(long long ctas_per_z, int nz) {
-  const long long target = 148LL * 8;
-  long long nzc = (target + ctas_per_z - 1) / ctas_per_z;
-  nzc = std::max(1LL, std::min(nzc, (long long)std::max(1, nz / 4)));
-  nzc = std::max(nzc, (long long)((nz + 63) / 64));
-  return (int)nzc;
+// Plane-kernel configuration: 3D uses 32x8 (x, y) tiles (two rows per thread except in the
+// fused Arnoldi modes); 2D uses 32 x-points x 8 right-hand sides. The ring depth S is a
+// launch parameter: the largest S <= 12 whose ring fits the shared-memory budget of
+// `occ_target` CTAs per SM (default 2; HELM_PLANE_OCC / HELM_PLANE_S override, for tuning).
+template <int MODE, bool YC> constexpr int plane_py() { return (YC && MODE < 3) ? 2 : 1; }
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+struct PlaneTune { int occ_target, s_fixed; };
+const PlaneTune& plane_tune() {
+  static const PlaneTune t{std::max(1, env_int("HELM_PLANE_OCC", 2)), env_int("HELM_PLANE_S", 0)};
+  return t;
+}
+
+struct PlaneCfg { int S = 0, occ = 0; size_t smem = 0; };
+
+// Launch with exactly one resident wave (groups x cpg CTAs, see stencil.cuh).
+template <typename R, int MODE, int NV, bool YC>
+void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
+  constexpr int PY = plane_py<MODE, YC>();
+  using Sh = PlaneShape<MODE, NV>;
+  constexpr int NT = 32 * 8 / PY;
+  constexpr size_t sb = PlaneSmem<R, 32, 8, Sh::NX, Sh::NP, YC>::stage_bytes;
+  auto kern = k_plane<R, 32, 8, PY, MODE, NV, YC>;
+  static const PlaneCfg cfg = [&] {
+    PlaneCfg c;
+    const PlaneTune& t = plane_tune();
+    c.S = t.s_fixed >= 4 ? std::min(t.s_fixed, 12) : (int)std::min<size_t>(12, (220 * 1024) / (t.occ_target * sb));
+    c.S = std::max(c.S, 4);
+    c.smem = c.S * sb;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ, kern, NT, c.smem));
+    if (c.occ < 1) throw HelmErr{HELM_ERR_STATE, "plane kernel does not fit on an SM"};
+    return c;
+  }();
+  const long long G = (long long)num_sms() * cfg.occ;
+  const long long minu = 4;   // at least 4 planes per CTA
+  long long cpg = std::max(1LL, std::min(G / groups, (units + minu - 1) / minu));
+  a.cpg = (int)cpg;
+  a.S = cfg.S;
+  kern<<<(unsigned)(groups * cpg), NT, cfg.smem, st>>>(a);
 }
 
 // Plane-streaming stencil (stencil.cuh). mode 0: y = s H x; 1: y = b - H x (+cycle start);
-// 2: y = s H x with the fused projections h_ij = <V_i, y>, i < nv (nv = j + 1).
-// 3D: 32x8 (x,y) tiles, one RHS per CTA; 2D: 32 x-points x 8 right-hand sides per CTA.
+// 2: y = s H x with the fused projections h_ij = <V_i, y>, i < nv (nv = j + 1);
+// 3: fused Arnoldi step nv of unpreconditioned GMRES (x = raw W or V_0, V = basis, vout);
+// 4: its last step (Y not stored, the last column finalised by Pythagoras).
 template <typename R>
 void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* x, cx<R>* y, const cx<R>* b,
-                  const VPtrs<R>* V, int nv, const double* xscale, const int* kact, int j, const KCtx& ctx) {
+                  const VPtrs<R>* V, int nv, const double* xscale, const int* kact, int j, const KCtx& ctx,
+                  cx<R>* vout = nullptr) {
   PlaneArgs<R> a{};
   a.g = geo<R>(op, l, adj);
-  a.x = x; a.y = y; a.b = b;
+  a.x = x; a.y = y; a.b = b; a.vout = vout;
   if (V) a.V = *V;
   a.xscale = xscale; a.sstride = K1; a.active = op->active_d; a.kact = kact; a.jstep = j;
+  a.jskip = mode >= 3 ? std::max(nv - 1, 0) : j;
   a.nrhs = nrhs; a.ctx = ctx; a.rb = op->rb;
   const bool d3 = a.g.ny > 1;
   a.ntx = (a.g.nx + 31) / 32;
-  a.nty = d3 ? (a.g.ny + 7) / 8 : (nrhs + 7) / 8;
-  const long long ctas_per_z = (long long)a.ntx * a.nty * (d3 ? nrhs : 1);
-  const int nzc0 = plane_nzc(ctas_per_z, a.g.nz);
-  a.zlen = (a.g.nz + nzc0 - 1) / nzc0;
-  const int nzc = (a.g.nz + a.zlen - 1) / a.zlen;
-  const dim3 grid((unsigned)ctas_per_z, (unsigned)nzc);
+  a.nty = d3 ? (a.g.ny + 7) / 8 : 1;
+  const int groups = d3 ? nrhs : (nrhs + 7) / 8;
+  const long long units = (long long)a.ntx * a.nty * a.g.nz;
   const int cls = mode == 0 ? KC_STENCIL : (mode == 1 ? KC_RESID : KC_DOTS);
   prof_begin(cls, op->st, l);
   if (d3) {
-    if (mode == 0) run_plane<R, 0, 0, true>(a, grid, op->st);
-    else if (mode == 1) run_plane<R, 1, 0, true>(a, grid, op->st);
-    else dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, true>(a, grid, op->st); });
+    if (mode == 0) run_plane<R, 0, 0, true>(a, groups, units, op->st);
+    else if (mode == 1) run_plane<R, 1, 0, true>(a, groups, units, op->st);
+    else if (mode == 2) dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, true>(a, groups, units, op->st); });
+    else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_plane<R, 3, decltype(c)::value, true>(a, groups, units, op->st); });
+    else dispatch_k0(nv, [&](auto c) { run_plane<R, 4, decltype(c)::value, true>(a, groups, units, op->st); });
   } else {
-    if (mode == 0) run_plane<R, 0, 0, false>(a, grid, op->st);
-    else if (mode == 1) run_plane<R, 1, 0, false>(a, grid, op->st);
-    else dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, false>(a, grid, op->st); });
+    if (mode == 0) run_plane<R, 0, 0, false>(a, groups, units, op->st);
+    else if (mode == 1) run_plane<R, 1, 0, false>(a, groups, units, op->st);
+    else if (mode == 2) dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, false>(a, groups, units, op->st); });
+    else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_plane<R, 3, decltype(c)::value, false>(a, groups, units, op->st); });
+    else dispatch_k0(nv, [&](auto c) { run_plane<R, 4, decltype(c)::value, false>(a, groups, units, op->st); });
   }
   CKL();
   const double Sc = sizeof(cx<R>), Sr = sizeof(R);
-  const double per = mode == 0 ? 2 * Sc + Sr : (mode == 1 ? 3 * Sc + Sr : (2 + nv) * Sc + Sr);
+  double per;
+  if (mode == 0) per = 2 * Sc + Sr;
+  else if (mode == 1) per = 3 * Sc + Sr;
+  else if (mode == 2) per = (2 + nv) * Sc + Sr;
+  else if (mode == 3) per = (nv == 0 ? 2 : nv + 3) * Sc + Sr;
+  else per = (nv == 0 ? 1 : nv + 2) * Sc + Sr;   // last step: Y is not stored
   prof_end(cls, op->st, acct(op, l, per * a.g.N, true, nrhs));
 }
 
@@ -398,12 +433,16 @@ void launch_prolong_add(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* ou
 // ------------------------------------------------------------------------------ Krylov
 // One restarted GMRES (flex = false) / FGMRES (flex = true, right preconditioner M) process
 // of `ko` cycles of `ki` Arnoldi steps on level l (fixed counts, R19; breakdown guard D14).
+// GMRES steps are fused (stencil.cuh MODE 3/4): step j forms v_j from the previous raw
+// product W and the basis while applying H, so there is no separate update pass; W
+// ping-pongs between V[ki] and Wx; the last step closes the Hessenberg by Pythagoras.
+// FGMRES keeps stencil+projections (MODE 2) + update (its v_{j+1} feeds the preconditioner).
 template <typename R>
 using Precond = std::function<void(const cx<R>* v, const double* vscale, const int* kact, int j, cx<R>* z)>;
 
 template <typename R>
 void krylov(helm_op* op, int l, int adj, int nrhs, KCtx& ctx, int ko, int ki, bool flex, const cx<R>* b,
-            cx<R>* x, bool x0zero, cx<R>* const* V, cx<R>* const* Z, const Precond<R>& M) {
+            cx<R>* x, bool x0zero, cx<R>* const* V, cx<R>* const* Z, const Precond<R>& M, cx<R>* Wx = nullptr) {
   ctx.k = ki;
   for (int cyc = 0; cyc < ko; ++cyc) {
     const bool first_zero = (cyc == 0 && x0zero);
@@ -415,29 +454,27 @@ void krylov(helm_op* op, int l, int adj, int nrhs, KCtx& ctx, int ko, int ki, bo
       launch_stencil<R>(op, l, adj, 1, nrhs, x, V[0], b, nullptr, nullptr, 0, ctx);
       v0 = V[0];
     }
-    for (int j = 0; j < ki; ++j) {
-      VPtrs<R> Vp = vptrs<R>(V, v0, j + 1);
-      const cx<R>* zj;
-      const double* zs;
-      if (flex) {
-        M(Vp.p[j], ctx.scale + j, ctx.kact, j, Z[j]);
-        zj = Z[j];
-        zs = nullptr;
-      } else {
-        zj = Vp.p[j];
-        zs = ctx.scale + j;
+    if (!flex) {
+      cx<R>* Wb[2] = {V[ki], Wx};
+      for (int j = 0; j < ki; ++j) {
+        VPtrs<R> Vp = vptrs<R>(V, v0, j);
+        const cx<R>* xin = j == 0 ? v0 : Wb[(j - 1) & 1];
+        launch_plane<R>(op, l, adj, j == ki - 1 ? 4 : 3, nrhs, xin, Wb[j & 1], nullptr, &Vp, j, nullptr, ctx.kact,
+                        j, ctx, j == 0 ? nullptr : V[j]);
       }
-      launch_plane<R>(op, l, adj, 2, nrhs, zj, V[j + 1], nullptr, &Vp, j + 1, zs, ctx.kact, j, ctx);
-      launch_update<R>(op, l, nrhs, Vp, j, V[j + 1], ctx);
-    }
-    if (flex) {
-      VPtrs<R> Zp{};
-      for (int i = 0; i < ki; ++i) Zp.p[i] = Z[i];
-      launch_solupdate<R>(op, l, nrhs, Zp, nullptr, x, first_zero, ki, ctx);
-    } else {
       VPtrs<R> Vp = vptrs<R>(V, v0, ki);
       launch_solupdate<R>(op, l, nrhs, Vp, ctx.scale, x, first_zero, ki, ctx);
+      continue;
     }
+    for (int j = 0; j < ki; ++j) {
+      VPtrs<R> Vp = vptrs<R>(V, v0, j + 1);
+      M(Vp.p[j], ctx.scale + j, ctx.kact, j, Z[j]);
+      launch_plane<R>(op, l, adj, 2, nrhs, Z[j], V[j + 1], nullptr, &Vp, j + 1, nullptr, ctx.kact, j, ctx);
+      launch_update<R>(op, l, nrhs, Vp, j, V[j + 1], ctx);
+    }
+    VPtrs<R> Zp{};
+    for (int i = 0; i < ki; ++i) Zp.p[i] = Z[i];
+    launch_solupdate<R>(op, l, nrhs, Zp, nullptr, x, first_zero, ki, ctx);
   }
 }
 
@@ -451,14 +488,14 @@ void vcycle(helm_op* op, int l, int adj, int nrhs, const cx<R>* b, cx<R>* x) {
   LevelWS<R>* W = wsets<R>(op);
   const helm_mlopts& o = op->ml;
   // pre-smooth: GMRES(ks_o, ks_i) from 0 (R19)
-  krylov<R>(op, l, adj, nrhs, W[l].ctxS, o.ks_o, o.ks_i, false, b, x, true, W[l].SV, nullptr, nullptr);
+  krylov<R>(op, l, adj, nrhs, W[l].ctxS, o.ks_o, o.ks_i, false, b, x, true, W[l].SV, nullptr, nullptr, W[l].SW);
   // residual and restriction (R = 2^-d P^T, R21)
   launch_stencil<R>(op, l, adj, 1, nrhs, x, W[l].SV[0], b, nullptr, nullptr, 0, W[l].ctxS);
   launch_restrict<R>(op, l, nrhs, W[l].SV[0], W[l + 1].Fb);
   // coarse solve (R20): coarsest GMRES, otherwise FGMRES preconditioned by V-cycle_{l+1}
   if (l + 1 == op->L - 1) {
     krylov<R>(op, l + 1, adj, nrhs, W[l + 1].ctxC, o.kc_o, o.kc_i, false, W[l + 1].Fb, W[l + 1].Fx, true,
-              W[l + 1].FV, nullptr, nullptr);
+              W[l + 1].FV, nullptr, nullptr, W[l + 1].FW);
   } else {
     Precond<R> M = [op, l, adj, nrhs, W](const cx<R>* v, const double* vs, const int* kact, int j, cx<R>* z) {
       launch_copy_scale<cx<R>, cx<R>>(op, l + 1, nrhs, v, W[l + 1].VB, vs, kact, j);
@@ -469,7 +506,7 @@ void vcycle(helm_op* op, int l, int adj, int nrhs, const cx<R>* b, cx<R>* x) {
   }
   launch_prolong_add<R>(op, l, nrhs, W[l + 1].Fx, x);
   // post-smooth: GMRES(ks_o, ks_i) from the current x
-  krylov<R>(op, l, adj, nrhs, W[l].ctxS, o.ks_o, o.ks_i, false, b, x, false, W[l].SV, nullptr, nullptr);
+  krylov<R>(op, l, adj, nrhs, W[l].ctxS, o.ks_o, o.ks_i, false, b, x, false, W[l].SV, nullptr, nullptr, W[l].SW);
 }
 
 // ------------------------------------------------------------------------------ setup
@@ -542,9 +579,10 @@ void alloc_ws(helm_op* op) {
     const double f = op->lev[l].N / N0 * (sizeof(cx<R>) / 16.0);
     if (l < op->L - 1) {   // levels that run a V-cycle: smoother basis + input copy
       for (int i = 0; i <= o.ks_i; ++i) W[l].SV[i] = dalloc<cx<R>>(op->allocs, n);
+      W[l].SW = dalloc<cx<R>>(op->allocs, n);
       W[l].VB = dalloc<cx<R>>(op->allocs, n);
       W[l].ctxS = make_ctx(op->allocs, B, o.ks_i);
-      vec += (o.ks_i + 2) * f;
+      vec += (o.ks_i + 3) * f;
       if (l == 0 && op->dtype == HELM_C64) { W[l].VX = dalloc<cx<R>>(op->allocs, n); vec += f; }
     }
     if (l >= 1) {          // coarse solves
@@ -552,10 +590,12 @@ void alloc_ws(helm_op* op) {
       const bool flex = (l < op->L - 1);
       if (flex)
         for (int i = 0; i < o.kc_i; ++i) W[l].FZ[i] = dalloc<cx<R>>(op->allocs, n);
+      else
+        W[l].FW = dalloc<cx<R>>(op->allocs, n);
       W[l].Fx = dalloc<cx<R>>(op->allocs, n);
       W[l].Fb = dalloc<cx<R>>(op->allocs, n);
       W[l].ctxC = make_ctx(op->allocs, B, o.kc_i);
-      vec += ((o.kc_i + 1) + (flex ? o.kc_i : 0) + 2) * f;
+      vec += ((o.kc_i + 1) + (flex ? o.kc_i : 1) + 2) * f;
     }
   }
   op->ws_vectors += vec;
@@ -649,17 +689,13 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
         }
   }
   op->m_int_d = dalloc<double>(op->allocs, n_int);
-  // reduction scratch: stencil residual partials (tiles x z-chunks) or BLAS (KMAX+1) x blocks
-  long long pst = (long long)K1 * TARGET_BLOCKS;
-  for (int l = 0; l < L; ++l) {
-    const LevelDev& Lv = op->lev[l];
-    const bool d3 = Lv.ny > 1;
-    const long long ntx = (Lv.nx + 31) / 32, nty = d3 ? (Lv.ny + 7) / 8 : 1;
-    const long long nzc_max = std::max(1, Lv.nz / 4) + (Lv.nz + 63) / 64 + 1;
-    pst = std::max(pst, (long long)K1 * ntx * nty * nzc_max * (d3 ? 4 : 1));
-  }
+  // reduction scratch: BLAS kernels use (KMAX+1) x blocks per RHS at stride pstride; the
+  // plane kernels use (KMAX+2) x slots per RHS, <= max(2048/32 x SMs, 8 x max_rhs) slots total
+  // (one resident wave of CTAs, one slot per warp, see run_plane).
+  const long long pst = (long long)K1 * TARGET_BLOCKS;
+  const long long plane_slots = std::max(64LL * num_sms(), 8LL * max_rhs) * (HELM_KMAX + 2);
   op->rb.pstride = pst;
-  op->rb.part = dalloc<double2>(op->allocs, (size_t)pst * max_rhs);
+  op->rb.part = dalloc<double2>(op->allocs, (size_t)std::max(pst * max_rhs, plane_slots));
   op->rb.ticket = dalloc<unsigned>(op->allocs, max_rhs);
   CK(cudaMemset(op->rb.ticket, 0, sizeof(unsigned) * max_rhs));
   op->active_d = dalloc<int>(op->allocs, max_rhs);
@@ -983,6 +1019,50 @@ void* level_ptr_check(const helm_op* op, int level) {
   return nullptr;
 }
 
+// Measurement probe: `reps` back-to-back launches of one hot-path kernel on the op's level
+// workspace (CUDA events on the stream; average ms per launch). kind 0-4 = plane modes
+// (nv = Krylov step), 10 = solution update (k = nv), 11 = CGS update (j = nv), 12 = norm.
+template <typename R>
+double probe_run(helm_op* op, int level, int kind, int nv, int nrhs, int reps) {
+  LevelWS<R>* W = wsets<R>(op);
+  LevelWS<R>& w = W[level];
+  const bool sm = level < op->L - 1;
+  cx<R>* const* V = sm ? w.SV : w.FV;
+  cx<R>* Wx = sm ? w.SW : (w.FW ? w.FW : w.Fx);
+  KCtx& ctx = sm ? w.ctxS : w.ctxC;
+  REQ(V[0] && Wx, HELM_ERR_STATE, "no workspace on this level");
+  const int k = sm ? op->ml.ks_i : op->ml.kc_i;
+  REQ(nv >= 0 && nv < k, HELM_ERR_ARG, "nv out of range");
+  const long long N = op->lev[level].N;
+  for (int i = 0; i <= k; ++i) CK(cudaMemsetAsync(V[i], 0x3f, sizeof(cx<R>) * N * nrhs, op->st));
+  CK(cudaMemsetAsync(Wx, 0x3f, sizeof(cx<R>) * N * nrhs, op->st));
+  ctx.k = k;
+  launch_norm_start<R>(op, level, nrhs, V[0], ctx);
+  VPtrs<R> Vp = vptrs<R>(V, V[0], std::max(nv, 1));
+  VPtrs<R> Vq = vptrs<R>(V, V[0], nv + 1);
+  auto one = [&] {
+    if (kind <= 4)
+      launch_plane<R>(op, level, 0, kind, nrhs, Wx, V[k], V[1], kind == 2 ? &Vq : &Vp, kind == 2 ? nv + 1 : nv,
+                      nullptr, ctx.kact, nv, ctx, kind >= 3 && nv > 0 ? V[nv] : nullptr);
+    else if (kind == 10) launch_solupdate<R>(op, level, nrhs, Vp, ctx.scale, Wx, 0, std::max(nv, 1), ctx);
+    else if (kind == 11) launch_update<R>(op, level, nrhs, Vq, nv, V[k], ctx);
+    else launch_norm_start<R>(op, level, nrhs, V[0], ctx);
+  };
+  one();
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, op->st));
+  for (int i = 0; i < reps; ++i) one();
+  CK(cudaEventRecord(e1, op->st));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ms / reps;
+}
+
 }  // namespace
 
 // ================================================================================ C ABI
@@ -1147,6 +1227,20 @@ helm_status helm_transfer(helm_op* op, int32_t level, int32_t prolong, int32_t n
       if (prolong) launch_prolong_add<float>(op, level, nrhs, (const float2*)in, (float2*)out);
       else launch_restrict<float>(op, level, nrhs, (const float2*)in, (float2*)out);
     }
+  });
+}
+
+helm_status helm_probe_kernel(helm_op* op, int32_t level, int32_t kind, int32_t nv, int32_t nrhs, int32_t reps,
+                              double* ms_per_launch, void* stream) {
+  return wrap([&] {
+    level_ptr_check(op, level);
+    REQ(!op->apply_only, HELM_ERR_STATE, "operator-only op");
+    REQ(nrhs >= 1 && nrhs <= op->max_rhs && reps >= 1 && ms_per_launch, HELM_ERR_ARG, "bad probe arguments");
+    op->st = (cudaStream_t)stream;
+    reset_acct(op, nrhs);
+    set_active(op, nrhs);
+    *ms_per_launch = op->dtype == HELM_C128 ? probe_run<double>(op, level, kind, nv, nrhs, reps)
+                                            : probe_run<float>(op, level, kind, nv, nrhs, reps);
   });
 }
 

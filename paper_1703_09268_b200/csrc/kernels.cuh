@@ -23,6 +23,53 @@ struct RedBuf {            // reduction scratch: partials per rhs + one ticket p
   long long pstride;       // double2 entries per rhs
 };
 
+// ================================================================= Krylov scalars (device)
+// Start a (re)started Krylov cycle of RHS r with ||r_0|| = beta: v_0 = r_0 / beta (lazy).
+__device__ inline void start_cycle(const KCtx& ctx, int r, double beta) {
+  constexpr int K1 = HELM_KMAX + 1;
+  ctx.beta[r] = beta;
+  ctx.scale[r * K1] = beta > 0.0 ? 1.0 / beta : 0.0;
+  for (int i = 0; i <= HELM_KMAX; ++i) ctx.g[r * K1 + i] = make_double2(i == 0 ? beta : 0.0, 0.0);
+  ctx.kact[r] = beta > 0.0 ? ctx.k : 0;
+}
+
+// Column j of the Hessenberg of RHS r is complete once h_{j+1,j} = hn is known: apply the
+// previous Givens rotations to it, form rotation j, rotate g (residual estimate |g_{j+1}|),
+// set the lazy scale of v_{j+1}, and apply the exact-breakdown guard (D14).
+__device__ inline void finalize_column(const KCtx& ctx, int r, int j, double hn) {
+  constexpr int K1 = HELM_KMAX + 1;
+  double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
+  double* cs = ctx.cs + r * HELM_KMAX;
+  double2* sn = ctx.sn + r * HELM_KMAX;
+  double2* gv = ctx.g + r * K1;
+  for (int i = 0; i < j; ++i) {   // previous rotations on column j
+    const double2 a = H[hidx(i, j)], bb = H[hidx(i + 1, j)];
+    const double c = cs[i];
+    const double2 sv = sn[i];
+    H[hidx(i, j)] = cadd(make_double2(c * a.x, c * a.y), cmul(sv, bb));
+    H[hidx(i + 1, j)] = csub(make_double2(c * bb.x, c * bb.y), cmul(cconj(sv), a));
+  }
+  const double2 a = H[hidx(j, j)];
+  const double aa = sqrt(cabs2(a)), rr = sqrt(aa * aa + hn * hn);
+  double c;
+  double2 sv;
+  if (rr == 0.0) { c = 1.0; sv = make_double2(0.0, 0.0); }
+  else if (aa == 0.0) { c = 0.0; sv = make_double2(1.0, 0.0); }
+  else { c = aa / rr; sv = make_double2(a.x / aa * hn / rr, a.y / aa * hn / rr); }
+  cs[j] = c; sn[j] = sv;
+  H[hidx(j, j)] = cadd(make_double2(c * a.x, c * a.y), make_double2(sv.x * hn, sv.y * hn));
+  H[hidx(j + 1, j)] = make_double2(0.0, 0.0);
+  const double2 gj = gv[j];
+  gv[j + 1] = cmul(make_double2(-sv.x, sv.y), gj);   // -conj(s) g_j
+  gv[j] = make_double2(c * gj.x, c * gj.y);
+  if (hn <= 1e-14 * ctx.beta[r]) {                    // breakdown guard (D14)
+    ctx.kact[r] = j + 1;
+    ctx.scale[r * K1 + j + 1] = 0.0;
+  } else {
+    ctx.scale[r * K1 + j + 1] = 1.0 / hn;
+  }
+}
+
 // ================================================================= a1: setup (D2-D4, D6, D13)
 struct AxisPml {
   int N;            // nodes on this level
@@ -122,123 +169,6 @@ __global__ void k_cast_c(long long n, const double2* __restrict__ a, float2* __r
   if (p < n) b[p] = make_float2((float)a[p].x, (float)a[p].y);
 }
 
-// ================================================================= a2 (+a5, a6): stencil
-// MODE 0: y = s_r * H x                      (s_r = xscale[r*sstride] or 1)
-// MODE 1: y = b - H x, and per-RHS ||y|| starts a Krylov cycle in ctx (beta, v0 scale, g, kact)
-// One CTA owns a BX x BY column tile and a z-range; it marches in z keeping x(z-1), x(z),
-// x(z+1) of its column in registers; the (x, y) neighbours of plane z come from a shared
-// plane with a one-point halo. PML enters only through the 1D tables (D4-D6).
-template <typename R, int BX, int BY, int MODE>
-__global__ void __launch_bounds__(BX * BY)
-k_stencil(Geo<R> g, const cx<R>* __restrict__ x, cx<R>* __restrict__ y, const cx<R>* __restrict__ b,
-          const double* __restrict__ xscale, int sstride, const int* __restrict__ active,
-          const int* __restrict__ kact, int jstep, int nrhs, int ntx, int nty, int zlen,
-          KCtx ctx, RedBuf rb) {
-  using C = cx<R>;
-  const int bid = blockIdx.x;
-  const int r = bid % nrhs, tile = bid / nrhs;
-  if (active && !active[r]) return;
-  if (kact && jstep >= kact[r]) return;
-  const int txb = tile % ntx, tyb = tile / ntx;
-  const int tx = threadIdx.x % BX, ty = threadIdx.x / BX;
-  const int ix = txb * BX + tx, iy = tyb * BY + ty;
-  const int nx = g.nx, ny = g.ny, nz = g.nz;
-  const int z0 = blockIdx.y * zlen, z1 = min(z0 + zlen, nz);
-  const bool valid = ix < nx && iy < ny;
-  const long long N = g.N, plane = (long long)nx * ny;
-  const C* xr = x + (long long)r * N;
-  C* yr = y + (long long)r * N;
-  const C* br = MODE == 1 ? b + (long long)r * N : nullptr;
-  const R s = (MODE == 0 && xscale) ? (R)xscale[(long long)r * sstride] : (R)1;
-  const C zero = mkc((R)0, (R)0);
-
-  __shared__ C sh[BY + 2][BX + 2];
-  C lox = zero, upx = zero, loy = zero, upy = zero, dxy = zero;
-  if (valid) {
-    lox = g.lo[0][ix]; upx = g.up[0][ix];
-    loy = g.lo[1][iy]; upy = g.up[1][iy];
-    dxy = cadd(g.dg[0][ix], g.dg[1][iy]);
-  }
-  const long long col = (long long)iy * nx + ix;
-  auto ld = [&](int xx, int yy, int zz) -> C {
-    if (xx < 0 || xx >= nx || yy < 0 || yy >= ny || zz < 0 || zz >= nz) return zero;
-    return xr[(long long)zz * plane + (long long)yy * nx + xx];
-  };
-  C below = zero, cur = zero, hxl = zero, hxr = zero, hyl = zero, hyr = zero;
-  if (valid) {
-    below = ld(ix, iy, z0 - 1);
-    cur = ld(ix, iy, z0);
-  }
-  if (iy < ny) {
-    if (tx == 0) hxl = ld(ix - 1, iy, z0);
-    if (tx == BX - 1) hxr = ld(ix + 1, iy, z0);
-  }
-  if (ix < nx) {
-    if (ty == 0) hyl = ld(ix, iy - 1, z0);
-    if (ty == BY - 1) hyr = ld(ix, iy + 1, z0);
-  }
-  double nrm = 0.0;
-  for (int z = z0; z < z1; ++z) {
-    // prefetch plane z+1 (centre and halo) into registers
-    C above = zero, nxl = zero, nxr = zero, nyl = zero, nyr = zero;
-    if (valid) above = ld(ix, iy, z + 1);
-    if (z + 1 < z1) {
-      if (iy < ny) {
-        if (tx == 0) nxl = ld(ix - 1, iy, z + 1);
-        if (tx == BX - 1) nxr = ld(ix + 1, iy, z + 1);
-      }
-      if (ix < nx) {
-        if (ty == 0) nyl = ld(ix, iy - 1, z + 1);
-        if (ty == BY - 1) nyr = ld(ix, iy + 1, z + 1);
-      }
-    }
-    sh[ty + 1][tx + 1] = cur;
-    if (tx == 0) sh[ty + 1][0] = hxl;
-    if (tx == BX - 1) sh[ty + 1][BX + 1] = hxr;
-    if (ty == 0) sh[0][tx + 1] = hyl;
-    if (ty == BY - 1) sh[BY + 1][tx + 1] = hyr;
-    __syncthreads();
-    if (valid) {
-      const long long p = (long long)z * plane + col;
-      const C lz = g.lo[2][z], uz = g.up[2][z], dz = g.dg[2][z];
-      const R wm = g.w2 * g.m[p];
-      C dia = mkc(dxy.x + dz.x + wm, dxy.y + dz.y);
-      C acc = cmul(dia, cur);
-      acc = cfma(lox, sh[ty + 1][tx], acc);
-      acc = cfma(upx, sh[ty + 1][tx + 2], acc);
-      acc = cfma(loy, sh[ty][tx + 1], acc);
-      acc = cfma(upy, sh[ty + 2][tx + 1], acc);
-      acc = cfma(lz, below, acc);
-      acc = cfma(uz, above, acc);
-      if (MODE == 0) {
-        yr[p] = cscale(acc, s);
-      } else {
-        C rv = csub(br[p], acc);
-        yr[p] = rv;
-        nrm += (double)rv.x * rv.x + (double)rv.y * rv.y;
-      }
-    }
-    __syncthreads();
-    below = cur; cur = above;
-    hxl = nxl; hxr = nxr; hyl = nyl; hyr = nyr;
-  }
-  if (MODE == 1) {
-    __shared__ double2 sm[32];
-    __shared__ double2 tot[1];
-    double2 v[1] = {make_double2(nrm, 0.0)};
-    const int blk = tile + ntx * nty * blockIdx.y, nblk = ntx * nty * gridDim.y;
-    if (grid_sum_last<1>(v, 1, rb.part + r * rb.pstride, rb.ticket + r, blk, nblk, sm, tot)) {
-      if (threadIdx.x == 0) {
-        const double beta = sqrt(tot[0].x);
-        ctx.beta[r] = beta;
-        ctx.scale[r * (HELM_KMAX + 1)] = beta > 0.0 ? 1.0 / beta : 0.0;
-        for (int i = 0; i <= HELM_KMAX; ++i) ctx.g[r * (HELM_KMAX + 1) + i] = make_double2(i == 0 ? beta : 0.0, 0.0);
-        ctx.kact[r] = beta > 0.0 ? ctx.k : 0;
-      }
-    }
-  }
-}
-
 // ================================================================= a3/a4: Krylov BLAS-1
 // Cycle start from x0 = 0: r = b, v0 = b / ||b|| (lazy: scale only).
 template <typename R>
@@ -256,154 +186,7 @@ k_norm_start(long long N, const cx<R>* __restrict__ b, const int* __restrict__ a
   __shared__ double2 tot[1];
   double2 v[1] = {make_double2(s, 0.0)};
   if (grid_sum_last<1>(v, 1, rb.part + r * rb.pstride, rb.ticket + r, blockIdx.x, gridDim.x, sm, tot)) {
-    if (threadIdx.x == 0) {
-      const double beta = sqrt(tot[0].x);
-      ctx.beta[r] = beta;
-      ctx.scale[r * (HELM_KMAX + 1)] = beta > 0.0 ? 1.0 / beta : 0.0;
-      for (int i = 0; i <= HELM_KMAX; ++i) ctx.g[r * (HELM_KMAX + 1) + i] = make_double2(i == 0 ? beta : 0.0, 0.0);
-      ctx.kact[r] = beta > 0.0 ? ctx.k : 0;
-    }
-  }
-}
-
-// Classical Gram-Schmidt projections h_ij = <v_i, w> = s_i <V_i, w>, i <= j (fp64 sums).
-template <typename R>
-__global__ void __launch_bounds__(HELM_RED_THREADS)
-k_dots(long long N, VPtrs<R> V, int j, const cx<R>* __restrict__ w, const int* __restrict__ active,
-       KCtx ctx, RedBuf rb) {
-  const int r = blockIdx.y;
-  if (active && !active[r]) return;
-  if (j >= ctx.kact[r]) return;
-  const long long off = (long long)r * N;
-  const cx<R>* wr = w + off;
-  double2 acc[HELM_KMAX + 1];
-#pragma unroll
-  for (int i = 0; i <= HELM_KMAX; ++i) acc[i] = make_double2(0.0, 0.0);
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
-    const double2 wv = to_d(wr[p]);
-#pragma unroll
-    for (int i = 0; i <= HELM_KMAX; ++i)
-      if (i <= j) acc[i] = cdot_acc(acc[i], to_d(V.p[i][off + p]), wv);
-  }
-  __shared__ double2 sm[32 * (HELM_KMAX + 1)];
-  __shared__ double2 tot[HELM_KMAX + 1];
-  if (grid_sum_last<HELM_KMAX + 1>(acc, j + 1, rb.part + r * rb.pstride, rb.ticket + r, blockIdx.x, gridDim.x, sm, tot)) {
-    if (threadIdx.x == 0) {
-      const double* sc = ctx.scale + r * (HELM_KMAX + 1);
-      double2* H = ctx.H + (long long)r * (HELM_KMAX + 1) * HELM_KMAX;
-      for (int i = 0; i <= j; ++i) H[hidx(i, j)] = make_double2(tot[i].x * sc[i], tot[i].y * sc[i]);
-    }
-  }
-}
-
-// w <- w - sum_i h_ij v_i (in place, w becomes V_{j+1} unnormalised), ||w||, then (last
-// block) h_{j+1,j}, Givens rotation of column j, residual estimate, breakdown guard (D14).
-template <typename R>
-__global__ void __launch_bounds__(HELM_RED_THREADS)
-k_update(long long N, VPtrs<R> V, int j, cx<R>* __restrict__ w, const int* __restrict__ active,
-         KCtx ctx, RedBuf rb) {
-  const int r = blockIdx.y;
-  if (active && !active[r]) return;
-  if (j >= ctx.kact[r]) return;
-  const long long off = (long long)r * N;
-  cx<R>* wr = w + off;
-  __shared__ cx<R> coef[HELM_KMAX + 1];
-  if (threadIdx.x <= j) {
-    const double2 h = ctx.H[(long long)r * (HELM_KMAX + 1) * HELM_KMAX + hidx(threadIdx.x, j)];
-    const double sc = ctx.scale[r * (HELM_KMAX + 1) + threadIdx.x];
-    coef[threadIdx.x] = from_d<cx<R>>(make_double2(-h.x * sc, -h.y * sc));
-  }
-  __syncthreads();
-  double s = 0.0;
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
-    cx<R> wv = wr[p];
-#pragma unroll
-    for (int i = 0; i <= HELM_KMAX; ++i)
-      if (i <= j) wv = cfma(coef[i], V.p[i][off + p], wv);
-    wr[p] = wv;
-    s += (double)wv.x * wv.x + (double)wv.y * wv.y;
-  }
-  __shared__ double2 sm[32];
-  __shared__ double2 tot[1];
-  double2 v[1] = {make_double2(s, 0.0)};
-  if (grid_sum_last<1>(v, 1, rb.part + r * rb.pstride, rb.ticket + r, blockIdx.x, gridDim.x, sm, tot)) {
-    if (threadIdx.x == 0) {
-      const int K1 = HELM_KMAX + 1;
-      double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
-      double* cs = ctx.cs + r * HELM_KMAX;
-      double2* sn = ctx.sn + r * HELM_KMAX;
-      double2* gv = ctx.g + r * K1;
-      const double hn = sqrt(tot[0].x);
-      H[hidx(j + 1, j)] = make_double2(hn, 0.0);
-      for (int i = 0; i < j; ++i) {   // previous rotations
-        const double2 a = H[hidx(i, j)], bb = H[hidx(i + 1, j)];
-        const double c = cs[i];
-        const double2 sv = sn[i];
-        H[hidx(i, j)] = cadd(make_double2(c * a.x, c * a.y), cmul(sv, bb));
-        H[hidx(i + 1, j)] = csub(make_double2(c * bb.x, c * bb.y), cmul(cconj(sv), a));
-      }
-      const double2 a = H[hidx(j, j)];
-      const double bn = hn;
-      const double aa = sqrt(cabs2(a)), rr = sqrt(aa * aa + bn * bn);
-      double c;
-      double2 sv;
-      if (rr == 0.0) { c = 1.0; sv = make_double2(0.0, 0.0); }
-      else if (aa == 0.0) { c = 0.0; sv = make_double2(1.0, 0.0); }
-      else { c = aa / rr; sv = make_double2(a.x / aa * bn / rr, a.y / aa * bn / rr); }
-      cs[j] = c; sn[j] = sv;
-      H[hidx(j, j)] = cadd(make_double2(c * a.x, c * a.y), make_double2(sv.x * bn, sv.y * bn));
-      H[hidx(j + 1, j)] = make_double2(0.0, 0.0);
-      const double2 gj = gv[j];
-      gv[j + 1] = cmul(make_double2(-sv.x, sv.y), gj);   // -conj(s) g_j
-      gv[j] = make_double2(c * gj.x, c * gj.y);
-      if (hn <= 1e-14 * ctx.beta[r]) {                    // breakdown guard (D14)
-        ctx.kact[r] = j + 1;
-        ctx.scale[r * K1 + j + 1] = 0.0;
-      } else {
-        ctx.scale[r * K1 + j + 1] = 1.0 / hn;
-      }
-    }
-  }
-}
-
-// x <- (init ? 0 : x) + sum_{i<kact} y_i z_i with R y = g (back substitution on the rotated
-// Hessenberg, per RHS, recomputed by every block), z_i = zs_i Z_i (zs = lazy scales or 1).
-template <typename R>
-__global__ void __launch_bounds__(HELM_RED_THREADS)
-k_solupdate(long long N, VPtrs<R> Z, const double* __restrict__ zscale, cx<R>* __restrict__ x, int init,
-            const int* __restrict__ active, KCtx ctx) {
-  const int r = blockIdx.y;
-  if (active && !active[r]) return;
-  __shared__ cx<R> yc[HELM_KMAX];
-  __shared__ int s_k;
-  if (threadIdx.x == 0) {
-    const int K1 = HELM_KMAX + 1;
-    const int k = ctx.kact[r];
-    const double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
-    const double2* gv = ctx.g + r * K1;
-    double2 yv[HELM_KMAX];
-    for (int i = k - 1; i >= 0; --i) {
-      double2 t = gv[i];
-      for (int l = i + 1; l < k; ++l) t = csub(t, cmul(H[hidx(i, l)], yv[l]));
-      yv[i] = cdiv(t, H[hidx(i, i)]);
-    }
-    for (int i = 0; i < k; ++i) {
-      const double sc = zscale ? zscale[r * K1 + i] : 1.0;
-      yc[i] = from_d<cx<R>>(make_double2(yv[i].x * sc, yv[i].y * sc));
-    }
-    s_k = k;
-  }
-  __syncthreads();
-  const int k = s_k;
-  if (k == 0 && !init) return;
-  const long long off = (long long)r * N;
-  cx<R>* xr = x + off;
-  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
-    cx<R> xv = init ? mkc((R)0, (R)0) : xr[p];
-#pragma unroll
-    for (int i = 0; i < HELM_KMAX; ++i)
-      if (i < k) xv = cfma(yc[i], Z.p[i][off + p], xv);
-    xr[p] = xv;
+    if (threadIdx.x == 0) start_cycle(ctx, r, sqrt(tot[0].x));
   }
 }
 
@@ -619,40 +402,7 @@ k_update_t(long long N, VPtrs<R> V, int j, cx<R>* __restrict__ w, const int* __r
   __shared__ double2 tot[1];
   double2 v[1] = {make_double2(s, 0.0)};
   if (grid_sum_last<1>(v, 1, rb.part + r * rb.pstride, rb.ticket + r, blockIdx.x, gridDim.x, sm, tot)) {
-    if (threadIdx.x == 0) {
-      const int K1 = HELM_KMAX + 1;
-      double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
-      double* cs = ctx.cs + r * HELM_KMAX;
-      double2* sn = ctx.sn + r * HELM_KMAX;
-      double2* gv = ctx.g + r * K1;
-      const double hn = sqrt(tot[0].x);
-      for (int i = 0; i < j; ++i) {   // previous rotations on column j
-        const double2 a = H[hidx(i, j)], bb = H[hidx(i + 1, j)];
-        const double c = cs[i];
-        const double2 sv = sn[i];
-        H[hidx(i, j)] = cadd(make_double2(c * a.x, c * a.y), cmul(sv, bb));
-        H[hidx(i + 1, j)] = csub(make_double2(c * bb.x, c * bb.y), cmul(cconj(sv), a));
-      }
-      const double2 a = H[hidx(j, j)];
-      const double aa = sqrt(cabs2(a)), rr = sqrt(aa * aa + hn * hn);
-      double c;
-      double2 sv;
-      if (rr == 0.0) { c = 1.0; sv = make_double2(0.0, 0.0); }
-      else if (aa == 0.0) { c = 0.0; sv = make_double2(1.0, 0.0); }
-      else { c = aa / rr; sv = make_double2(a.x / aa * hn / rr, a.y / aa * hn / rr); }
-      cs[j] = c; sn[j] = sv;
-      H[hidx(j, j)] = cadd(make_double2(c * a.x, c * a.y), make_double2(sv.x * hn, sv.y * hn));
-      H[hidx(j + 1, j)] = make_double2(0.0, 0.0);
-      const double2 gj = gv[j];
-      gv[j + 1] = cmul(make_double2(-sv.x, sv.y), gj);   // -conj(s) g_j
-      gv[j] = make_double2(c * gj.x, c * gj.y);
-      if (hn <= 1e-14 * ctx.beta[r]) {                    // breakdown guard (D14)
-        ctx.kact[r] = j + 1;
-        ctx.scale[r * K1 + j + 1] = 0.0;
-      } else {
-        ctx.scale[r * K1 + j + 1] = 1.0 / hn;
-      }
-    }
+    if (threadIdx.x == 0) finalize_column(ctx, r, j, sqrt(tot[0].x));
   }
 }
 

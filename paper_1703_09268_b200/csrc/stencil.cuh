@@ -1,21 +1,28 @@
-// stencil.cuh — pipelined plane-streaming stencil for sm_100a (a2, and a3's projections).
+// stencil.cuh — pipelined plane-streaming stencil for sm_100a (a2, and a3's fused Arnoldi).
 //
-// A CTA owns a BX x BY tile of "rows" and a z-range, and streams the planes z0-1 .. z1 of
-// its input through an S-stage shared-memory ring filled by asynchronous copies (cp.async /
-// LDGSTS; zero-fill implements the Dirichlet ghosts, R7): the tile plus its one-point halo,
-// the model m and, per mode, the own-point operands (b for the residual, V_0..V_{NV-1} for
-// the fused Gram-Schmidt projections). S-3 planes stay in flight while plane z is computed
-// (Little's law: ~40 KB in flight per SM at ~800 ns keeps HBM streaming).
-//   YC = true  (3D): rows are y (coupled by the stencil), one RHS per CTA.
-//   YC = false (2D): rows are right-hand sides (uncoupled); the grid plane is one x-row,
-//                    so every sync still covers BX*BY points.
-// Each thread owns PY rows of one column; per-thread load slots (global offset, shared
-// offset, static predicate) are computed once and advanced by one plane per step. PML
-// enters only through the 1D tables (D4-D6).
+// Work decomposition. A "row tile" is BX x BY rows of the extended grid: (x, y) points of
+// one RHS in 3D (YC = true), or 32 x-points of 8 right-hand sides in 2D (YC = false; rows
+// are uncoupled RHS and the plane is one x-row). A unit of work is one (row tile, z plane).
+// The grid is exactly one resident wave: `groups` x `cpg` CTAs, where a group is one RHS
+// (3D) or one 8-RHS row group (2D) and its T*nz units are split into cpg equal contiguous
+// ranges. A CTA walks its range as segments (maximal runs inside one row tile) and streams
+// the planes z0-1 .. z1 of each segment through an S-stage shared-memory ring filled by
+// asynchronous copies (cp.async / LDGSTS; zero-fill implements the Dirichlet ghosts, R7):
+// the tile plus its one-point halo for every halo'd operand, the model m, the per-plane
+// z coefficients of the 1D tables and, per mode, the own-point operands. S-3 planes are in
+// flight while plane z is computed. No wave tail, no per-plane global-latency bubble.
+// PML enters only through the 1D tables (D4-D6).
 //
 // MODE 0: y = s H x              (s = lazy normalisation of x, per RHS)
 // MODE 1: y = b - H x, ||y||     (starts a Krylov cycle: beta, v0 scale, g, kact)
-// MODE 2: w = s H x and h_i = <V_i, w>, i < NV (fused CGS projections, fp64 sums)
+// MODE 2: w = s H x and h_i = <V_i, w>, i < NV (fused CGS projections, fp64 sums) — FGMRES
+// MODE 3/4: fused Arnoldi step NV of unpreconditioned GMRES (lazy normalisation; 4 = last):
+//           NV = 0: Y = H V_0,                          dots <V_0, Y>
+//           NV > 0: V_NV = s_{NV-1} W - sum_{i<NV} h_{i,NV-1} s_i V_i formed on the fly
+//                   (halo included) from the raw W = Y_{NV-1} and V_0..V_{NV-1};
+//                   writes V_NV and Y = H V_NV; dots <V_i, Y>, i <= NV, and ||V_NV||^2.
+//         The last CTA per RHS finalises column NV-1 (h_{NV,NV-1} = ||V_NV||, Givens,
+//         breakdown guard) and stores column NV: h_{i,NV} = s_i s_NV <V_i, Y>.
 #pragma once
 #include "kernels.cuh"
 
@@ -28,29 +35,57 @@ template <int B> __device__ __forceinline__ void cpa(unsigned s, const void* gme
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+// wait until at most n groups are pending (n is block-uniform; wait_group needs an immediate)
+__device__ __forceinline__ void cpa_wait_n(int n) {
+  switch (n) {
+    case 0: cpa_wait<0>(); break;   case 1: cpa_wait<1>(); break;   case 2: cpa_wait<2>(); break;
+    case 3: cpa_wait<3>(); break;   case 4: cpa_wait<4>(); break;   case 5: cpa_wait<5>(); break;
+    case 6: cpa_wait<6>(); break;   case 7: cpa_wait<7>(); break;   case 8: cpa_wait<8>(); break;
+    case 9: cpa_wait<9>(); break;   case 10: cpa_wait<10>(); break; default: cpa_wait<11>(); break;
+  }
+}
 
 template <typename R> struct PlaneArgs {
   Geo<R> g;
-  const cx<R>* x;          // input (rhs-major)
+  const cx<R>* x;          // halo'd input: x (MODE 0-2); V_0 (MODE 3, NV = 0) or raw W (MODE 3, NV > 0)
   cx<R>* y;                // output
   const cx<R>* b;          // MODE 1
-  VPtrs<R> V;              // MODE 2
+  VPtrs<R> V;              // MODE 2: own-point V_0..V_{NV-1}; MODE 3: halo'd V_0..V_{NV-1}
+  cx<R>* vout;             // MODE 3 (NV > 0): the formed V_NV is written here
   const double* xscale;    // MODE 0/2: per-RHS lazy scale of x (stride sstride) or null
   int sstride;
   const int* active;       // per-RHS outer mask or null
-  const int* kact;         // skip RHS r if jstep >= kact[r] (null = never)
-  int jstep;
-  int nrhs, ntx, nty, zlen;
+  const int* kact;         // skip RHS r if jskip >= kact[r] (null = never)
+  int jskip;
+  int jstep;               // Hessenberg column written (MODE 2, 3)
+  int nrhs, ntx, nty;      // row tiles: ntx x nty per group (nty = 1 in 2D)
+  int cpg;                 // CTAs per group
+  int S;                   // ring stages (>= 4)
   KCtx ctx;
   RedBuf rb;
 };
 
-template <typename R, int BX, int BY, int NP>
+template <typename R, int BX, int BY, int NX, int NP, bool YC>
 struct PlaneSmem {
-  static constexpr int XE = (BY + 2) * (BX + 2);    // halo tile elements
+  static constexpr int YH = YC ? 1 : 0;              // y-halo rows (3D only)
+  static constexpr int XE = (BY + 2 * YH) * (BX + 2); // halo tile elements
   static constexpr int PE = BY * BX;                 // own-point elements
-  static constexpr size_t stage_bytes =
-      ((XE * sizeof(cx<R>) + PE * sizeof(R) + NP * PE * sizeof(cx<R>)) + 127) / 128 * 128;
+  static constexpr size_t x_off = 0;
+  static constexpr size_t m_off = (size_t)NX * XE * sizeof(cx<R>);
+  static constexpr size_t p_off = m_off + PE * sizeof(R);
+  static constexpr size_t z_off = p_off + (size_t)NP * PE * sizeof(cx<R>);
+  static constexpr size_t stage_bytes = (z_off + 3 * sizeof(cx<R>) + 127) / 128 * 128;
+};
+
+// MODE 4 = MODE 3 for the LAST step of a cycle: Y = H V_NV is not stored, and ||Y||^2 is
+// reduced too, so that h_{NV+1,NV} = (s_NV^2 ||Y||^2 - sum_i |h_{i,NV}|^2)^{1/2}
+// (Pythagoras on the orthonormal basis) finalises the last column without another pass
+// over the data. V_{NV+1} itself is never needed; this h only enters the last Givens
+// rotation (and the unused residual estimate), where its rounding is negligible.
+template <int MODE, int NV> struct PlaneShape {
+  static constexpr int NX = MODE >= 3 ? NV + 1 : 1;                       // halo'd tiles
+  static constexpr int NP = MODE == 1 ? 1 : (MODE == 2 ? NV : 0);         // own-point operands
+  static constexpr int NVR = MODE == 1 ? 1 : (MODE == 2 ? NV : (MODE >= 3 ? NV + 3 : 1));
 };
 
 // Deterministic warp-level reduction into per-RHS slots: lane 0 of each contributing warp
@@ -99,222 +134,316 @@ __device__ __forceinline__ bool warp_slot_reduce(double2 (&v)[NV], double2* part
   return true;
 }
 
-template <typename R, int BX, int BY, int PY, int S, int MODE, int NV, bool YC>
+template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC>
 __global__ void __launch_bounds__(BX * BY / PY)
 k_plane(const PlaneArgs<R> a) {
   using C = cx<R>;
-  constexpr int NP = MODE == 1 ? 1 : (MODE == 2 ? NV : 0);
-  constexpr int NVR = MODE == 1 ? 1 : (MODE == 2 ? NV : 1);   // reduced values per RHS
-  using SM = PlaneSmem<R, BX, BY, NP>;
+  using Sh = PlaneShape<MODE, NV>;
+  constexpr int NX = Sh::NX, NP = Sh::NP, NVR = Sh::NVR;
+  using SM = PlaneSmem<R, BX, BY, NX, NP, YC>;
+  constexpr int YH = SM::YH;
   constexpr int NT = BX * BY / PY;
   constexpr int RS = BY / PY;          // row stride between a thread's rows
   constexpr int XP = BX + 2;           // shared row pitch (elements)
+  constexpr bool FORM = MODE >= 3 && NV > 0;
+  constexpr bool LAST = MODE == 4;
   static_assert(YC || PY == 1, "2D (rows = RHS) uses one row per thread");
   static_assert(BX == 32, "one warp per tile row");
   extern __shared__ __align__(128) unsigned char smem[];
 
   const Geo<R>& g = a.g;
+  const int S = a.S;
   const int nx = g.nx, ny = g.ny, nz = g.nz;
   const int tx = threadIdx.x % BX, ty0 = threadIdx.x / BX;
-  int tile = blockIdx.x, r0 = 0;
-  if constexpr (YC) {
-    r0 = blockIdx.x % a.nrhs;
-    tile = blockIdx.x / a.nrhs;
-    if (a.active && !a.active[r0]) return;
-    if (a.kact && a.jstep >= a.kact[r0]) return;
-  }
-  const int txb = tile % a.ntx, tyb = tile / a.ntx;
-  const int ix = txb * BX + tx;
-  const int z0 = blockIdx.y * a.zlen, z1 = min(z0 + a.zlen, nz);
+  const int grp = blockIdx.x / a.cpg, cig = blockIdx.x % a.cpg;
   const long long N = g.N;
   const long long plane = YC ? (long long)nx * ny : (long long)nx;
   const C zero = mkc((R)0, (R)0);
 
-  // ---- rows owned by this thread: spatial y (YC) or right-hand side (2D)
-  int rowv[PY];          // y index (YC) or rhs index (2D)
-  bool rok[PY];          // row exists, is active, and this lane's column is inside the grid
-  bool ract = true;      // 2D: this warp's RHS row exists and is active (warp-uniform)
-  R sc[PY];              // lazy scale of x for this row's RHS
-  long long gofs[PY];    // global offset of (ix, row) at z = 0
+  // ---- rows of this thread: its RHS (3D: the group; 2D: group*BY + row)
+  int rhs[PY];
+  bool ract = true;      // this thread's RHS exists and is active (warp-uniform in 2D)
+  R sc = (R)1;           // lazy scale of x for this thread's RHS (MODE 0 / 2)
+  if constexpr (YC) {
+    const int r = grp;
+    if (a.active && !a.active[r]) return;
+    if (a.kact && a.jskip >= a.kact[r]) return;
 #pragma unroll
-  for (int k = 0; k < PY; ++k) {
-    const int row = tyb * BY + ty0 + k * RS;
-    rowv[k] = row;
-    if constexpr (YC) {
-      rok[k] = row < ny && ix < nx;
-      gofs[k] = (long long)r0 * N + (long long)row * nx + ix;
-      sc[k] = (MODE != 1 && a.xscale) ? (R)a.xscale[(long long)r0 * a.sstride] : (R)1;
-    } else {
-      bool ok = row < a.nrhs;
-      if (ok && a.active && !a.active[row]) ok = false;
-      if (ok && a.kact && a.jstep >= a.kact[row]) ok = false;
-      ract = ok;
-      rok[k] = ok && ix < nx;
-      gofs[k] = (long long)min(row, a.nrhs - 1) * N + ix;
-      sc[k] = (ok && MODE != 1 && a.xscale) ? (R)a.xscale[(long long)row * a.sstride] : (R)1;
-    }
-  }
-  if constexpr (!YC) {
+    for (int k = 0; k < PY; ++k) rhs[k] = r;
+  } else {
+    const int r = grp * BY + ty0;
+    bool ok = r < a.nrhs;
+    if (ok && a.active && !a.active[r]) ok = false;
+    if (ok && a.kact && a.jskip >= a.kact[r]) ok = false;
+    ract = ok;
+    rhs[0] = ok ? r : 0;
     if (!__syncthreads_or(ract ? 1 : 0)) return;
   }
+  if ((MODE == 0 || MODE == 2) && a.xscale && ract) sc = (R)a.xscale[(long long)rhs[0] * a.sstride];
 
-  // ---- load slots: own points, x-halo, y-halo (YC) — fixed per thread, bumped per plane
-  constexpr int NL = 2 * PY + (YC ? 2 : 0);
-  long long lg[NL];
-  unsigned ls[NL];
-  bool lp[NL];
-  int nl = 0;
+  // ---- MODE 3 forming coefficients of this thread's RHS: V_NV = cw W + sum_i cv_i V_i
+  R cw = (R)1;
+  C cv[FORM ? NV : 1];
+  if constexpr (FORM) {
+    const int r = rhs[0];
+    const double* s = a.ctx.scale + (long long)r * (HELM_KMAX + 1);
+    const double2* H = a.ctx.H + (long long)r * (HELM_KMAX + 1) * HELM_KMAX;
+    cw = (R)s[NV - 1];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double2 h = H[hidx(i, NV - 1)];
+      cv[i] = mkc((R)(-h.x * s[i]), (R)(-h.y * s[i]));
+    }
+  }
+
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
-#pragma unroll
-  for (int k = 0; k < PY; ++k) {
-    const int sr = ty0 + k * RS + 1;
-    lg[nl] = gofs[k]; ls[nl] = (unsigned)((sr * XP + tx + 1) * sizeof(C)); lp[nl] = rok[k]; ++nl;
-  }
-#pragma unroll
-  for (int k = 0; k < PY; ++k) {
-    const int sr = ty0 + k * RS + 1;
-    if (tx == 0) { lg[nl] = gofs[k] - 1; ls[nl] = (unsigned)(sr * XP * sizeof(C)); lp[nl] = rok[k] && ix > 0; ++nl; }
-    if (tx == BX - 1) { lg[nl] = gofs[k] + 1; ls[nl] = (unsigned)((sr * XP + BX + 1) * sizeof(C)); lp[nl] = rok[k] && ix + 1 < nx; ++nl; }
-  }
-  if constexpr (YC) {
-    if (ty0 == 0) {
-      lg[nl] = gofs[0] - nx; ls[nl] = (unsigned)((tx + 1) * sizeof(C)); lp[nl] = ix < nx && rowv[0] - 1 >= 0 && rowv[0] - 1 < ny; ++nl;
-    }
-    if (ty0 + (PY - 1) * RS == BY - 1) {
-      lg[nl] = gofs[PY - 1] + nx; ls[nl] = (unsigned)(((BY + 1) * XP + tx + 1) * sizeof(C));
-      lp[nl] = ix < nx && rowv[PY - 1] + 1 < ny; ++nl;
-    }
-  }
-  const long long mofs0 = YC ? (long long)rowv[0] * nx + ix : (long long)ix;
-  const unsigned m_s0 = (unsigned)(SM::XE * sizeof(C));
-  const unsigned p_s0 = (unsigned)(SM::XE * sizeof(C) + SM::PE * sizeof(R));
-
-  const int nq = z1 - z0 + 2;
-  auto load = [&](int q) {
-    if (q < nq) {
-      const int z = z0 - 1 + q;
-      const bool zin = z >= 0 && z < nz;
-      const unsigned st = sbase + (unsigned)((q % S) * SM::stage_bytes);
-      const long long zo = (long long)z * plane;
-#pragma unroll
-      for (int i = 0; i < NL; ++i)
-        if (i < nl) {
-          const bool p = lp[i] && zin;
-          cpa<sizeof(C)>(st + ls[i], p ? a.x + lg[i] + zo : a.x, p);
-        }
-      if (q >= 1 && z < z1) {
-#pragma unroll
-        for (int k = 0; k < PY; ++k)
-          if (rok[k]) {
-            const int pr = (ty0 + k * RS) * BX + tx;
-            cpa<sizeof(R)>(st + m_s0 + pr * sizeof(R), g.m + (YC ? mofs0 + (long long)k * RS * nx : mofs0) + zo, true);
-            if constexpr (MODE == 1) cpa<sizeof(C)>(st + p_s0 + pr * sizeof(C), a.b + gofs[k] + zo, true);
-            if constexpr (MODE == 2) {
-#pragma unroll
-              for (int v = 0; v < NV; ++v)
-                cpa<sizeof(C)>(st + p_s0 + (v * SM::PE + pr) * sizeof(C), a.V.p[v] + gofs[k] + zo, true);
-            }
-          }
-      }
-    }
-    cpa_commit();   // always commit (possibly empty) so group counting stays uniform
-  };
-
-  // ---- per-thread operator coefficients (1D tables; ghosts masked, R7)
-  const C lox = (ix > 0 && ix < nx) ? g.lo[0][ix] : zero;
-  const C upx = (ix < nx - 1) ? g.up[0][ix] : zero;
-  const C dgx = ix < nx ? g.dg[0][ix] : zero;
-  C loy[PY], upy[PY], dgy[PY];
-#pragma unroll
-  for (int k = 0; k < PY; ++k) {
-    if constexpr (YC) {
-      const int iy = rowv[k];
-      loy[k] = (iy > 0 && iy < ny) ? g.lo[1][iy] : zero;
-      upy[k] = (iy < ny - 1) ? g.up[1][iy] : zero;
-      dgy[k] = iy < ny ? g.dg[1][iy] : zero;
-    } else {
-      loy[k] = upy[k] = dgy[k] = zero;
-    }
-  }
-  double nrm = 0.0;
   double2 acc[NVR];
 #pragma unroll
   for (int k = 0; k < NVR; ++k) acc[k] = make_double2(0.0, 0.0);
+  double nrm = 0.0, ynrm = 0.0;
 
-#pragma unroll
-  for (int q = 0; q < S - 1; ++q) load(q);
-  for (int z = z0; z < z1; ++z) {
-    const int q = z - z0 + 1;
-    cpa_wait<S - 4>();        // this thread's groups <= q+1 complete (committed: <= q+S-3)
-    __syncthreads();          // ... for every thread; stage (q-2)%S is free again
-    load(q + S - 2);          // S-3 planes in flight while plane z is computed
-    const C* X0 = reinterpret_cast<const C*>(smem + ((q - 1) % S) * SM::stage_bytes);
-    const C* X1 = reinterpret_cast<const C*>(smem + (q % S) * SM::stage_bytes);
-    const C* X2 = reinterpret_cast<const C*>(smem + ((q + 1) % S) * SM::stage_bytes);
-    const R* Ms = reinterpret_cast<const R*>(smem + (q % S) * SM::stage_bytes + m_s0);
-    const C* Ps = reinterpret_cast<const C*>(smem + (q % S) * SM::stage_bytes + p_s0);
-    const C lz = z > 0 ? g.lo[2][z] : zero, uz = z < nz - 1 ? g.up[2][z] : zero, dz = g.dg[2][z];
-    const long long zo = (long long)z * plane;
+  const long long T = (long long)a.ntx * a.nty;
+  const long long U = T * nz;
+  long long u = (U * cig) / a.cpg;
+  const long long u1 = (U * (cig + 1)) / a.cpg;
+
+  while (u < u1) {
+    const int tile = (int)(u / nz);
+    const int z0 = (int)(u % nz);
+    const int z1 = (int)min((long long)nz, z0 + (u1 - u));
+    u += z1 - z0;
+    const int txb = tile % a.ntx, tyb = tile / a.ntx;
+    const int ix = txb * BX + tx;
+
+    int rowv[PY];
+    bool rok[PY];
+    long long gofs[PY];
 #pragma unroll
     for (int k = 0; k < PY; ++k) {
-      if (!rok[k]) continue;
-      const int c = (ty0 + k * RS + 1) * XP + tx + 1;
-      const int pr = (ty0 + k * RS) * BX + tx;
-      const C cur = X1[c];
-      const R wm = g.w2 * Ms[pr];
-      // tree-shaped sum: four independent complex products, then two adds
-      C t0 = cmul(mkc(dgx.x + dgy[k].x + dz.x + wm, dgx.y + dgy[k].y + dz.y), cur);
-      C t1 = cfma(upx, X1[c + 1], cmul(lox, X1[c - 1]));
-      C t2 = cfma(uz, X2[c], cmul(lz, X0[c]));
-      if constexpr (YC) t0 = cfma(upy[k], X1[c + XP], cfma(loy[k], X1[c - XP], t0));
-      const C hx = cadd(cadd(t0, t1), t2);
-      C* yp = a.y + gofs[k] + zo;
-      if constexpr (MODE == 0) {
-        *yp = cscale(hx, sc[k]);
-      } else if constexpr (MODE == 1) {
-        const C rv = csub(Ps[pr], hx);
-        *yp = rv;
-        nrm += (double)rv.x * rv.x + (double)rv.y * rv.y;
+      if constexpr (YC) {
+        const int row = tyb * BY + ty0 + k * RS;
+        rowv[k] = row;
+        rok[k] = row < ny && ix < nx;
+        gofs[k] = (long long)rhs[0] * N + (long long)row * nx + ix;
       } else {
-        const C w = cscale(hx, sc[k]);
-        *yp = w;
-        const double2 wd = to_d(w);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = cdot_acc(acc[v], to_d(Ps[v * SM::PE + pr]), wd);
+        rowv[k] = 0;
+        rok[k] = ract && ix < nx;
+        gofs[k] = (long long)rhs[0] * N + ix;
       }
     }
+    // load slots at fixed positions (static indexing keeps them in registers): own points
+    // [0, PY), x-halo left [PY, 2PY), right [2PY, 3PY), y-halo low / high (YC); `lh` says
+    // whether this thread issues the slot at all, `lp` whether it is in the grid (else the
+    // copy zero-fills: the Dirichlet ghost).
+    constexpr int NL = 3 * PY + (YC ? 2 : 0);
+    long long lg[NL];
+    unsigned ls[NL];
+    bool lp[NL], lh[NL];
+#pragma unroll
+    for (int k = 0; k < PY; ++k) {
+      const int sr = ty0 + k * RS + YH;
+      lg[k] = gofs[k]; ls[k] = (unsigned)((sr * XP + tx + 1) * sizeof(C)); lp[k] = rok[k]; lh[k] = true;
+      lg[PY + k] = gofs[k] - 1; ls[PY + k] = (unsigned)(sr * XP * sizeof(C));
+      lp[PY + k] = rok[k] && ix > 0; lh[PY + k] = tx == 0;
+      lg[2 * PY + k] = gofs[k] + 1; ls[2 * PY + k] = (unsigned)((sr * XP + BX + 1) * sizeof(C));
+      lp[2 * PY + k] = rok[k] && ix + 1 < nx; lh[2 * PY + k] = tx == BX - 1;
+    }
+    if constexpr (YC) {
+      lg[3 * PY] = gofs[0] - nx; ls[3 * PY] = (unsigned)((tx + 1) * sizeof(C));
+      lp[3 * PY] = ix < nx && rowv[0] - 1 >= 0 && rowv[0] - 1 < ny; lh[3 * PY] = ty0 == 0;
+      lg[3 * PY + 1] = gofs[PY - 1] + nx; ls[3 * PY + 1] = (unsigned)(((BY + 1) * XP + tx + 1) * sizeof(C));
+      lp[3 * PY + 1] = ix < nx && rowv[PY - 1] + 1 < ny; lh[3 * PY + 1] = ty0 + (PY - 1) * RS == BY - 1;
+    }
+    const long long mofs0 = YC ? (long long)rowv[0] * nx + ix : (long long)ix;
+
+    const int nq = z1 - z0 + 2;
+    auto load = [&](int q) {
+      if (q < nq) {
+        const int z = z0 - 1 + q;
+        const bool zin = z >= 0 && z < nz;
+        const unsigned st = sbase + (unsigned)((q % S) * SM::stage_bytes);
+        const long long zo = (long long)z * plane;
+#pragma unroll
+        for (int t = 0; t < NX; ++t) {
+          const C* src = t == 0 ? a.x : a.V.p[t - 1];
+#pragma unroll
+          for (int i = 0; i < NL; ++i)
+            if (lh[i]) {
+              const bool p = lp[i] && zin;
+              cpa<sizeof(C)>(st + (unsigned)(t * SM::XE * sizeof(C)) + ls[i], p ? src + lg[i] + zo : a.x, p);
+            }
+        }
+        if (q >= 1 && z < z1) {
+          if (threadIdx.x < 3) {   // z coefficients of plane z: lo, dg, up (ghosts masked, R7)
+            const C* tz = threadIdx.x == 0 ? g.lo[2] : (threadIdx.x == 1 ? g.dg[2] : g.up[2]);
+            const bool p = threadIdx.x == 1 || (threadIdx.x == 0 ? z > 0 : z < nz - 1);
+            cpa<sizeof(C)>(st + (unsigned)(SM::z_off + threadIdx.x * sizeof(C)), p ? tz + z : tz, p);
+          }
+#pragma unroll
+          for (int k = 0; k < PY; ++k)
+            if (rok[k]) {
+              const int pr = (ty0 + k * RS) * BX + tx;
+              cpa<sizeof(R)>(st + (unsigned)(SM::m_off + pr * sizeof(R)), g.m + (YC ? mofs0 + (long long)k * RS * nx : mofs0) + zo, true);
+              if constexpr (MODE == 1) cpa<sizeof(C)>(st + (unsigned)(SM::p_off + pr * sizeof(C)), a.b + gofs[k] + zo, true);
+              if constexpr (MODE == 2) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+                  cpa<sizeof(C)>(st + (unsigned)(SM::p_off + (v * SM::PE + pr) * sizeof(C)), a.V.p[v] + gofs[k] + zo, true);
+              }
+            }
+        }
+      }
+      cpa_commit();   // always commit (possibly empty) so group counting stays uniform
+    };
+    // MODE 3: turn the raw W tile of stage `q` into V_NV in place (halo included)
+    auto form = [&](int q) {
+      if constexpr (FORM) {
+        C* X = reinterpret_cast<C*>(smem + (q % S) * SM::stage_bytes);
+        auto f1 = [&](int e) {
+          C v = cscale(X[e], cw);
+#pragma unroll
+          for (int i = 0; i < NV; ++i) v = cfma(cv[i], X[(i + 1) * SM::XE + e], v);
+          X[e] = v;
+        };
+        if constexpr (YC) {
+          for (int e = threadIdx.x; e < SM::XE; e += NT) f1(e);
+        } else {
+          const int rowe = ty0 * XP;
+          f1(rowe + tx + 1);
+          if (tx == 0) f1(rowe);
+          if (tx == BX - 1) f1(rowe + BX + 1);
+        }
+      }
+    };
+
+    // per-thread operator coefficients along x (and y in 3D)
+    const C lox = (ix > 0 && ix < nx) ? g.lo[0][ix] : zero;
+    const C upx = (ix < nx - 1) ? g.up[0][ix] : zero;
+    const C dgx = ix < nx ? g.dg[0][ix] : zero;
+    C loy[PY], upy[PY], dgy[PY];
+#pragma unroll
+    for (int k = 0; k < PY; ++k) {
+      if constexpr (YC) {
+        const int iy = rowv[k];
+        loy[k] = (iy > 0 && iy < ny) ? g.lo[1][iy] : zero;
+        upy[k] = (iy < ny - 1) ? g.up[1][iy] : zero;
+        dgy[k] = iy < ny ? g.dg[1][iy] : zero;
+      } else {
+        loy[k] = upy[k] = dgy[k] = zero;
+      }
+    }
+
+    for (int q = 0; q < S - 1; ++q) load(q);
+    for (int z = z0; z < z1; ++z) {
+      const int q = z - z0 + 1;
+      cpa_wait_n(S - 4);        // this thread's groups <= q+1 complete (committed: <= q+S-3)
+      __syncthreads();          // ... for every thread; stage (q-2)%S is free again
+      load(q + S - 2);          // S-3 planes in flight while plane z is computed
+      if constexpr (FORM) {
+        if (z == z0) { form(q - 1); form(q); }
+        form(q + 1);
+        __syncthreads();
+      }
+      const unsigned char* st1 = smem + (q % S) * SM::stage_bytes;
+      const C* X0 = reinterpret_cast<const C*>(smem + ((q - 1) % S) * SM::stage_bytes);
+      const C* X1 = reinterpret_cast<const C*>(st1);
+      const C* X2 = reinterpret_cast<const C*>(smem + ((q + 1) % S) * SM::stage_bytes);
+      const R* Ms = reinterpret_cast<const R*>(st1 + SM::m_off);
+      const C* Ps = reinterpret_cast<const C*>(st1 + SM::p_off);
+      const C* Zt = reinterpret_cast<const C*>(st1 + SM::z_off);
+      const C lz = Zt[0], dz = Zt[1], uz = Zt[2];
+      const long long zo = (long long)z * plane;
+#pragma unroll
+      for (int k = 0; k < PY; ++k) {
+        if (!rok[k]) continue;
+        const int c = (ty0 + k * RS + YH) * XP + tx + 1;
+        const int pr = (ty0 + k * RS) * BX + tx;
+        const C cur = X1[c];
+        const R wm = g.w2 * Ms[pr];
+        // tree-shaped sum: four independent complex products, then two adds
+        C t0 = cmul(mkc(dgx.x + dgy[k].x + dz.x + wm, dgx.y + dgy[k].y + dz.y), cur);
+        C t1 = cfma(upx, X1[c + 1], cmul(lox, X1[c - 1]));
+        C t2 = cfma(uz, X2[c], cmul(lz, X0[c]));
+        if constexpr (YC) t0 = cfma(upy[k], X1[c + XP], cfma(loy[k], X1[c - XP], t0));
+        const C hx = cadd(cadd(t0, t1), t2);
+        C* yp = a.y + gofs[k] + zo;
+        if constexpr (MODE == 0) {
+          *yp = cscale(hx, sc);
+        } else if constexpr (MODE == 1) {
+          const C rv = csub(Ps[pr], hx);
+          *yp = rv;
+          nrm += (double)rv.x * rv.x + (double)rv.y * rv.y;
+        } else if constexpr (MODE == 2) {
+          const C w = cscale(hx, sc);
+          *yp = w;
+          const double2 wd = to_d(w);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[v] = cdot_acc(acc[v], to_d(Ps[v * SM::PE + pr]), wd);
+        } else {
+          const double2 hd = to_d(hx);
+          if constexpr (LAST) ynrm += hd.x * hd.x + hd.y * hd.y;
+          else *yp = hx;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) acc[v] = cdot_acc(acc[v], to_d(X1[(v + 1) * SM::XE + c]), hd);
+          acc[NV] = cdot_acc(acc[NV], to_d(cur), hd);
+          if constexpr (NV > 0) {
+            a.vout[gofs[k] + zo] = cur;
+            nrm += (double)cur.x * cur.x + (double)cur.y * cur.y;
+          }
+        }
+      }
+    }
+    cpa_wait<0>();
+    __syncthreads();   // the next segment's prologue reuses the ring
   }
-  cpa_wait<0>();
+
   if constexpr (MODE != 0) {
     if constexpr (MODE == 1) acc[0] = make_double2(nrm, 0.0);
-    // 3D: every warp of the CTA belongs to RHS r0 -> slots (tile, zchunk, warp)
-    // 2D: warp w owns RHS rowv[0]              -> slots (x-tile, zchunk)
+    if constexpr (MODE >= 3) acc[NV + 1] = make_double2(nrm, 0.0);
+    if constexpr (MODE >= 3) acc[NV + 2] = make_double2(ynrm, 0.0);
+    // 3D: every warp of the CTA belongs to RHS grp -> slots (cta in group, warp)
+    // 2D: warp w owns RHS grp*BY + w                -> slots (cta in group)
     int r, slot, nslots;
     if constexpr (YC) {
-      r = r0;
+      r = grp;
       constexpr int WPB = NT / 32;
-      slot = ((tile + a.ntx * a.nty * blockIdx.y) * WPB) + (threadIdx.x >> 5);
-      nslots = a.ntx * a.nty * gridDim.y * WPB;
+      slot = cig * WPB + (threadIdx.x >> 5);
+      nslots = a.cpg * WPB;
     } else {
-      r = rowv[0];
+      r = rhs[0];
       if (!ract) return;          // warp-uniform: one RHS row per warp
-      slot = txb + a.ntx * blockIdx.y;
-      nslots = a.ntx * gridDim.y;
+      slot = cig;
+      nslots = a.cpg;
     }
     double2 tot[NVR];
-    if (warp_slot_reduce<NVR>(acc, a.rb.part + r * a.rb.pstride, a.rb.ticket + r, slot, nslots, tot)) {
+    if (warp_slot_reduce<NVR>(acc, a.rb.part + (size_t)r * nslots * NVR, a.rb.ticket + r, slot, nslots, tot)) {
       if ((threadIdx.x & 31) == 0) {
+        const KCtx& ctx = a.ctx;
+        const int K1 = HELM_KMAX + 1;
         if constexpr (MODE == 1) {
-          const double beta = sqrt(tot[0].x);
-          KCtx ctx = a.ctx;
-          ctx.beta[r] = beta;
-          ctx.scale[r * (HELM_KMAX + 1)] = beta > 0.0 ? 1.0 / beta : 0.0;
-          for (int i = 0; i <= HELM_KMAX; ++i) ctx.g[r * (HELM_KMAX + 1) + i] = make_double2(i == 0 ? beta : 0.0, 0.0);
-          ctx.kact[r] = beta > 0.0 ? ctx.k : 0;
-        } else {
-          const double* scl = a.ctx.scale + r * (HELM_KMAX + 1);
-          double2* H = a.ctx.H + (long long)r * (HELM_KMAX + 1) * HELM_KMAX;
+          start_cycle(ctx, r, sqrt(tot[0].x));
+        } else if constexpr (MODE == 2) {
+          const double* scl = ctx.scale + r * K1;
+          double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
           for (int i = 0; i < NV; ++i) H[hidx(i, a.jstep)] = make_double2(tot[i].x * scl[i], tot[i].y * scl[i]);
+        } else {
+          if constexpr (NV > 0) finalize_column(ctx, r, NV - 1, sqrt(tot[NV + 1].x));
+          const double* scl = ctx.scale + r * K1;
+          const double sj = scl[NV];
+          double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
+          double hh = 0.0;
+          for (int i = 0; i <= NV; ++i) {
+            const double f = scl[i] * sj;
+            const double2 h = make_double2(tot[i].x * f, tot[i].y * f);
+            H[hidx(i, NV)] = h;
+            hh += cabs2(h);
+          }
+          if constexpr (LAST) {
+            if (NV < ctx.kact[r]) {   // column NV is live (no breakdown above)
+              const double w2 = sj * sj * tot[NV + 2].x;
+              finalize_column(ctx, r, NV, sqrt(fmax(w2 - hh, 0.0)));
+            }
+          }
         }
       }
     }

@@ -40,4 +40,14 @@ elif what == "cfg2":
     X = torch.empty_like(B)
     api.helm_solve(op, B, X, opts=api.SolveOpts(max_outer=1))
     torch.cuda.synchronize()
+elif what == "probe":
+    # python scripts/ncu_targets.py probe cfg2|mv256 level kind nv  (5 launches of one kernel)
+    case, level, kind, nv = sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
+    if case == "cfg2":
+        p, f, vref, nrhs = synth.cfg2(freqs=(5.0,)), 5.0, 3000.0, 50
+    else:
+        p, f, vref, nrhs = synth.cfg5(256), 6.0, 4500.0, 1
+    op = api.helm_setup(api.Grid.of(p), p.m, 2 * np.pi * f, api.Pml(v_ref=vref), api.C128, max_rhs=nrhs)
+    print(api.probe_kernel(op, level, kind, nv, nrhs, reps=4))
+    torch.cuda.synchronize()
 print("ok")

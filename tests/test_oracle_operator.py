@@ -150,3 +150,17 @@ def test_extension_identities():
     # E^T sums each PML line into its boundary cell: column sums count replicas
     cs = np.asarray(E.sum(axis=0)).ravel().reshape(p.m.shape)
     assert cs[2, 2, 2] == 1 and cs[0, 0, 0] == (1 + 3) ** 3
+
+
+@pytest.mark.parametrize("ndim", [2, 3])
+def test_slab_rows_equal_full_assembly(ndim):
+    """helmholtz_rows (used to check large grids slab by slab) = the pinned full D5 matrix
+    restricted to those z-planes, exactly."""
+    p = _prob(ndim, (11, 9, 10), 4)
+    w, pml = 2 * np.pi * 6, D.PmlParams(v_ref=2500.0)
+    H = D.helmholtz_matrix(p, w, pml)
+    Nx, Ny, Nz = p.next
+    for z0, z1 in ((0, 2), (5, 9), (Nz - 3, Nz)):
+        Hs = D.helmholtz_rows(p, w, pml, z0, z1)
+        ref = H[z0 * Ny * Nx:z1 * Ny * Nx]
+        assert (Hs - ref).count_nonzero() == 0 or abs(Hs - ref).max() == 0.0
