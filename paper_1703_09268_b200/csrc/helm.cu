@@ -2,7 +2,7 @@
 // level hierarchy, Krylov workspace), the FGMRES / ML-GMRES orchestration and the C ABI
 // declared in include/helm.h. All numerics run in the kernels of kernels.cuh.
 #include "helm.h"
-#include "stencil.cuh"
+#include "march2d.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -157,7 +157,10 @@ struct helm_op {
   helm_mlopts ml{};
   helm_dtype dtype = HELM_C128;
   int max_rhs = 1;
-  double omega = 0.0;
+  double omega = 0.0;          // = omegas[0]
+  int nop = 1;                 // operators (frequencies) sharing the geometry (joint batches)
+  double omegas[HELM_MAXOP] = {};
+  int* rop_d = nullptr;        // per-RHS operator index (device, max_rhs)
   double vref = 0.0;
   int L = 1;
   int dim = 3;
@@ -169,14 +172,15 @@ struct helm_op {
   double2* OX = nullptr;
   double2* OB = nullptr;
   KCtx ctxO{};
-  int* active_d = nullptr;
+  int* active_d = nullptr;     // compact list of the active RHS indices (nact entries)
+  int nact = 0;
   RedBuf rb{};
   double* m_int_d = nullptr;     // interior model (fp64)
   std::vector<void*> allocs;
   cudaStream_t st = nullptr;
   int k_inner = 5;
   // accounting (per RHS of the current solve)
-  std::vector<int> act_h;
+  std::vector<int> act_h, alist_h;
   std::vector<double> bytes;
   std::vector<int64_t> mv[4];
   double ws_vectors = 0.0;
@@ -226,7 +230,8 @@ template <> Geo<double> geo<double>(const helm_op* op, int l, int adj) {
   const LevelDev& L = op->lev[l];
   Geo<double> g{};
   g.nx = L.nx; g.ny = L.ny; g.nz = L.nz; g.N = L.N;
-  g.m = L.m64; g.w2 = op->omega * op->omega;
+  g.m = L.m64; g.nop = op->nop; g.rop = op->nop > 1 ? op->rop_d : nullptr;
+  for (int o = 0; o < op->nop; ++o) g.w2[o] = op->omegas[o] * op->omegas[o];
   for (int a = 0; a < 3; ++a) { g.lo[a] = L.t64[adj][a][0]; g.dg[a] = L.t64[adj][a][1]; g.up[a] = L.t64[adj][a][2]; }
   return g;
 }
@@ -234,7 +239,8 @@ template <> Geo<float> geo<float>(const helm_op* op, int l, int adj) {
   const LevelDev& L = op->lev[l];
   Geo<float> g{};
   g.nx = L.nx; g.ny = L.ny; g.nz = L.nz; g.N = L.N;
-  g.m = L.m32; g.w2 = (float)(op->omega * op->omega);
+  g.m = L.m32; g.nop = op->nop; g.rop = op->nop > 1 ? op->rop_d : nullptr;
+  for (int o = 0; o < op->nop; ++o) g.w2[o] = (float)(op->omegas[o] * op->omegas[o]);
   for (int a = 0; a < 3; ++a) { g.lo[a] = L.t32[adj][a][0]; g.dg[a] = L.t32[adj][a][1]; g.up[a] = L.t32[adj][a][2]; }
   return g;
 }
@@ -258,10 +264,10 @@ template <int N = 0, typename F> void dispatch_k0(int k, F&& f) {
   }
 }
 
-// Plane-kernel configuration: 3D uses 32x8 (x, y) tiles (two rows per thread except in the
-// fused Arnoldi modes); 2D uses 32 x-points x 8 right-hand sides. The ring depth S is a
-// launch parameter: the largest S <= 12 whose ring fits the shared-memory budget of
-// `occ_target` CTAs per SM (default 2; HELM_PLANE_OCC / HELM_PLANE_S override, for tuning).
+// Plane-kernel configuration: 32x8 row tiles, one row per thread (3D: x,y of one RHS; 2D:
+// 32 x-points x 8 right-hand sides). The ring depth S is a launch parameter: the largest
+// S <= 12 whose ring fits the shared-memory budget of `occ_target` CTAs per SM (default 4;
+// HELM_PLANE_OCC / HELM_PLANE_S override, for tuning).
 template <int MODE, bool YC> constexpr int plane_py() { return (YC && MODE < 3) ? 2 : 1; }
 
 int env_int(const char* name, int dflt) {
@@ -270,11 +276,29 @@ int env_int(const char* name, int dflt) {
 }
 struct PlaneTune { int occ_target, s_fixed; };
 const PlaneTune& plane_tune() {
-  static const PlaneTune t{std::max(1, env_int("HELM_PLANE_OCC", 2)), env_int("HELM_PLANE_S", 0)};
+  static const PlaneTune t{std::max(1, env_int("HELM_PLANE_OCC", 4)), env_int("HELM_PLANE_S", 0)};
   return t;
 }
 
 struct PlaneCfg { int S = 0, occ = 0; size_t smem = 0; };
+
+// Split of a group's T tiles x nz planes over its CTAs (one resident wave of G CTAs over
+// all groups): the z-chunk count minimising waves x (chunk planes + 2 halo planes).
+struct PlaneSplit { int cpg, nzc, zlen; };
+PlaneSplit plane_split(int groups, long long G, int T, int nz) {
+  const long long cpg0 = std::max(1LL, G / groups);
+  long long best = -1;
+  PlaneSplit r{1, 1, nz};
+  for (int n = 1; n <= nz; ++n) {
+    const int zl = (nz + n - 1) / n, nzc = (nz + zl - 1) / zl;
+    if (nzc != n) continue;
+    const long long items = (long long)T * nzc;
+    const long long waves = (items + cpg0 - 1) / cpg0;
+    const long long cost = waves * (zl + 2);
+    if (best < 0 || cost < best) { best = cost; r = PlaneSplit{(int)std::min(cpg0, items), nzc, zl}; }
+  }
+  return r;
+}
 
 // Launch with exactly one resident wave (groups x cpg CTAs, see stencil.cuh).
 template <typename R, int MODE, int NV, bool YC>
@@ -295,12 +319,98 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
     if (c.occ < 1) throw HelmErr{HELM_ERR_STATE, "plane kernel does not fit on an SM"};
     return c;
   }();
-  const long long G = (long long)num_sms() * cfg.occ;
-  const long long minu = 4;   // at least 4 planes per CTA
-  long long cpg = std::max(1LL, std::min(G / groups, (units + minu - 1) / minu));
-  a.cpg = (int)cpg;
+  const PlaneSplit sp = plane_split(groups, (long long)num_sms() * cfg.occ, a.ntx * a.nty, a.g.nz);
+  a.cpg = sp.cpg; a.nzc = sp.nzc; a.zlen = sp.zlen;
   a.S = cfg.S;
+  const long long cpg = sp.cpg;
   kern<<<(unsigned)(groups * cpg), NT, cfg.smem, st>>>(a);
+}
+
+// 2D: register z-march kernel (march2d.cuh), one warp per (RHS, 30-point strip, z-chunk)
+// item; exactly one resident wave of warps, split evenly over the right-hand sides.
+// Register prefetch depth (planes). Measured on B200 (scripts/tune_plane.py): deeper
+// prefetch of many operands costs occupancy faster than it adds bytes in flight, so the
+// multi-operand modes keep P = 2.
+template <typename R, int MODE, int NV> constexpr int march_p() {
+  if constexpr (MODE == 0) return sizeof(R) == 4 ? 8 : 6;
+  if constexpr (MODE == 1) return sizeof(R) == 4 ? 6 : 4;
+  return NV <= 1 ? 3 : 2;
+}
+
+template <typename R, int MODE, int NV>
+void run_march(MarchArgs<R>& a, cudaStream_t st) {
+  constexpr int P = march_p<R, MODE, NV>();
+  auto kern = k_march2d<R, MODE, NV, P>;
+  const size_t zs = (size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>);
+  static int occ = 0;
+  static size_t zs_max = 0;
+  if (zs > zs_max) {   // occupancy for the largest z-table seen so far
+    if (zs > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zs));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, zs));
+    if (occ < 1) throw HelmErr{HELM_ERR_STATE, "march kernel does not fit on an SM"};
+    zs_max = zs;
+    if (env_int("HELM_DEBUG", 0)) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kern);
+      std::fprintf(stderr, "[helm] march2d R=%zu mode=%d nv=%d P=%d regs=%d occ=%d warps/SM=%d\n", sizeof(R), MODE, NV,
+                   P, fa.numRegs, occ, occ * 4);
+    }
+  }
+  const long long W = (long long)num_sms() * occ * 4;
+  const int wpr = (int)std::max(1LL, W / a.nrhs);
+  const int nz = a.g.nz;
+  long long best = -1;
+  int nzc_b = 1, zl_b = nz;
+  for (int n = 1; n <= nz; ++n) {
+    const int zl = (nz + n - 1) / n, nzc = (nz + zl - 1) / zl;
+    if (nzc != n) continue;
+    const long long items = (long long)a.nstrip * nzc;
+    const long long cost = ((items + wpr - 1) / wpr) * (zl + 2 + P);
+    if (best < 0 || cost < best) { best = cost; nzc_b = nzc; zl_b = zl; }
+  }
+  a.nzc = nzc_b; a.zlen = zl_b;
+  a.wpr = (int)std::min<long long>(wpr, (long long)a.nstrip * nzc_b);
+  const long long warps = (long long)a.nrhs * a.wpr;
+  kern<<<(unsigned)((warps + 3) / 4), 128, zs, st>>>(a);
+}
+
+// 3D y = s H x: register z-march with RY y-rows per warp (march2d.cuh k_march3d).
+template <typename R, int RY>
+void run_march3d(March3Args<R>& a, cudaStream_t st) {
+  constexpr int P = (RY >= 4 && sizeof(R) == 8) ? 1 : 2;
+  auto kern = k_march3d<R, RY, P>;
+  const size_t zs = (size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>);
+  static int occ = 0;
+  static size_t zs_max = 0;
+  if (zs > zs_max) {
+    if (zs > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zs));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, zs));
+    if (occ < 1) throw HelmErr{HELM_ERR_STATE, "march3d kernel does not fit on an SM"};
+    zs_max = zs;
+    if (env_int("HELM_DEBUG", 0)) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kern);
+      std::fprintf(stderr, "[helm] march3d R=%zu RY=%d P=%d regs=%d occ=%d warps/SM=%d\n", sizeof(R), RY, P, fa.numRegs,
+                   occ, occ * 4);
+    }
+  }
+  const long long W = (long long)num_sms() * occ * 4;
+  const int wpr = (int)std::max(1LL, W / a.nrhs);
+  a.nyb = (a.g.ny + RY - 1) / RY;
+  const long long per_z = (long long)a.nyb * a.nstrip;
+  const int nz = a.g.nz;
+  long long best = -1;
+  int nzc_b = 1, zl_b = nz;
+  for (int n = 1; n <= nz; ++n) {
+    const int zl = (nz + n - 1) / n, nzc = (nz + zl - 1) / zl;
+    if (nzc != n) continue;
+    const long long cost = ((per_z * nzc + wpr - 1) / wpr) * (zl + 2 + P);
+    if (best < 0 || cost < best) { best = cost; nzc_b = nzc; zl_b = zl; }
+  }
+  a.nzc = nzc_b; a.zlen = zl_b;
+  a.wpr = (int)std::min<long long>(wpr, per_z * nzc_b);
+  const long long warps = (long long)a.nrhs * a.wpr;
+  kern<<<(unsigned)((warps + 3) / 4), 128, zs, st>>>(a);
 }
 
 // Plane-streaming stencil (stencil.cuh). mode 0: y = s H x; 1: y = b - H x (+cycle start);
@@ -311,34 +421,8 @@ template <typename R>
 void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* x, cx<R>* y, const cx<R>* b,
                   const VPtrs<R>* V, int nv, const double* xscale, const int* kact, int j, const KCtx& ctx,
                   cx<R>* vout = nullptr) {
-  PlaneArgs<R> a{};
-  a.g = geo<R>(op, l, adj);
-  a.x = x; a.y = y; a.b = b; a.vout = vout;
-  if (V) a.V = *V;
-  a.xscale = xscale; a.sstride = K1; a.active = op->active_d; a.kact = kact; a.jstep = j;
-  a.jskip = mode >= 3 ? std::max(nv - 1, 0) : j;
-  a.nrhs = nrhs; a.ctx = ctx; a.rb = op->rb;
-  const bool d3 = a.g.ny > 1;
-  a.ntx = (a.g.nx + 31) / 32;
-  a.nty = d3 ? (a.g.ny + 7) / 8 : 1;
-  const int groups = d3 ? nrhs : (nrhs + 7) / 8;
-  const long long units = (long long)a.ntx * a.nty * a.g.nz;
+  if (!op->nact) return;
   const int cls = mode == 0 ? KC_STENCIL : (mode == 1 ? KC_RESID : KC_DOTS);
-  prof_begin(cls, op->st, l);
-  if (d3) {
-    if (mode == 0) run_plane<R, 0, 0, true>(a, groups, units, op->st);
-    else if (mode == 1) run_plane<R, 1, 0, true>(a, groups, units, op->st);
-    else if (mode == 2) dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, true>(a, groups, units, op->st); });
-    else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_plane<R, 3, decltype(c)::value, true>(a, groups, units, op->st); });
-    else dispatch_k0(nv, [&](auto c) { run_plane<R, 4, decltype(c)::value, true>(a, groups, units, op->st); });
-  } else {
-    if (mode == 0) run_plane<R, 0, 0, false>(a, groups, units, op->st);
-    else if (mode == 1) run_plane<R, 1, 0, false>(a, groups, units, op->st);
-    else if (mode == 2) dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, false>(a, groups, units, op->st); });
-    else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_plane<R, 3, decltype(c)::value, false>(a, groups, units, op->st); });
-    else dispatch_k0(nv, [&](auto c) { run_plane<R, 4, decltype(c)::value, false>(a, groups, units, op->st); });
-  }
-  CKL();
   const double Sc = sizeof(cx<R>), Sr = sizeof(R);
   double per;
   if (mode == 0) per = 2 * Sc + Sr;
@@ -346,6 +430,56 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
   else if (mode == 2) per = (2 + nv) * Sc + Sr;
   else if (mode == 3) per = (nv == 0 ? 2 : nv + 3) * Sc + Sr;
   else per = (nv == 0 ? 1 : nv + 2) * Sc + Sr;   // last step: Y is not stored
+  if (op->lev[l].ny == 1) {   // 2D: register z-march
+    MarchArgs<R> m{};
+    m.g = geo<R>(op, l, adj);
+    m.x = x; m.y = y; m.b = b; m.vout = vout;
+    if (V) m.V = *V;
+    m.xscale = xscale; m.sstride = K1; m.active = op->active_d; m.kact = kact; m.jstep = j;
+    m.jskip = mode >= 3 ? std::max(nv - 1, 0) : j;
+    m.nrhs = op->nact; m.ctx = ctx; m.rb = op->rb;
+    m.nstrip = (m.g.nx + 29) / 30;
+    prof_begin(cls, op->st, l);
+    if (mode == 0) run_march<R, 0, 0>(m, op->st);
+    else if (mode == 1) run_march<R, 1, 0>(m, op->st);
+    else if (mode == 2) dispatch_k(nv, [&](auto c) { run_march<R, 2, decltype(c)::value>(m, op->st); });
+    else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_march<R, 3, decltype(c)::value>(m, op->st); });
+    else dispatch_k0(nv, [&](auto c) { run_march<R, 4, decltype(c)::value>(m, op->st); });
+    CKL();
+    prof_end(cls, op->st, acct(op, l, per * m.g.N, true, nrhs));
+    return;
+  }
+  static const int mv3d_ry = env_int("HELM_MV3D_RY", 0);
+  if (mode == 0 && mv3d_ry > 0) {   // 3D matvec: register z-march
+    March3Args<R> m{};
+    m.g = geo<R>(op, l, adj);
+    m.x = x; m.y = y; m.xscale = xscale; m.sstride = K1; m.active = op->active_d; m.nrhs = op->nact;
+    m.nstrip = (m.g.nx + 29) / 30;
+    prof_begin(cls, op->st, l);
+    if (mv3d_ry == 2) run_march3d<R, 2>(m, op->st);
+    else run_march3d<R, 4>(m, op->st);
+    CKL();
+    prof_end(cls, op->st, acct(op, l, per * m.g.N, true, nrhs));
+    return;
+  }
+  PlaneArgs<R> a{};
+  a.g = geo<R>(op, l, adj);
+  a.x = x; a.y = y; a.b = b; a.vout = vout;
+  if (V) a.V = *V;
+  a.xscale = xscale; a.sstride = K1; a.active = op->active_d; a.kact = kact; a.jstep = j;
+  a.jskip = mode >= 3 ? std::max(nv - 1, 0) : j;
+  a.nrhs = nrhs; a.ctx = ctx; a.rb = op->rb;
+  a.ntx = (a.g.nx + 31) / 32;
+  a.nty = (a.g.ny + 7) / 8;
+  const int groups = op->nact;
+  const long long units = (long long)a.ntx * a.nty * a.g.nz;
+  prof_begin(cls, op->st, l);
+  if (mode == 0) run_plane<R, 0, 0, true>(a, groups, units, op->st);
+  else if (mode == 1) run_plane<R, 1, 0, true>(a, groups, units, op->st);
+  else if (mode == 2) dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, true>(a, groups, units, op->st); });
+  else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_plane<R, 3, decltype(c)::value, true>(a, groups, units, op->st); });
+  else dispatch_k0(nv, [&](auto c) { run_plane<R, 4, decltype(c)::value, true>(a, groups, units, op->st); });
+  CKL();
   prof_end(cls, op->st, acct(op, l, per * a.g.N, true, nrhs));
 }
 
@@ -364,7 +498,8 @@ template <typename R> VPtrs<R> vptrs(cx<R>* const* V, const cx<R>* v0, int n) {
 template <typename R>
 void launch_norm_start(helm_op* op, int l, int nrhs, const cx<R>* b, const KCtx& ctx) {
   const long long N = op->lev[l].N;
-  dim3 grid(blas_blocks(N, nrhs), nrhs);
+  if (!op->nact) return;
+  dim3 grid(blas_blocks(N, op->nact), op->nact);
   prof_begin(KC_NORM, op->st, l);
   k_norm_start<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, b, op->active_d, ctx, op->rb);
   CKL();
@@ -374,7 +509,8 @@ void launch_norm_start(helm_op* op, int l, int nrhs, const cx<R>* b, const KCtx&
 template <typename R>
 void launch_update(helm_op* op, int l, int nrhs, const VPtrs<R>& V, int j, cx<R>* w, const KCtx& ctx) {
   const long long N = op->lev[l].N;
-  dim3 grid(blas_blocks(N, nrhs), nrhs);
+  if (!op->nact) return;
+  dim3 grid(blas_blocks(N, op->nact), op->nact);
   prof_begin(KC_UPDATE, op->st, l);
   dispatch_k(j + 1, [&](auto c) {
     k_update_t<R, decltype(c)::value><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, V, j, w, op->active_d, ctx, op->rb);
@@ -387,7 +523,8 @@ template <typename R>
 void launch_solupdate(helm_op* op, int l, int nrhs, const VPtrs<R>& Z, const double* zscale, cx<R>* x,
                       int init, int k, const KCtx& ctx) {
   const long long N = op->lev[l].N;
-  dim3 grid(blas_blocks(N, nrhs), nrhs);
+  if (!op->nact) return;
+  dim3 grid(blas_blocks(N, op->nact), op->nact);
   prof_begin(KC_SOLUPD, op->st, l);
   dispatch_k(k, [&](auto c) {
     k_solupdate_t<R, decltype(c)::value><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, Z, zscale, x, init, op->active_d, ctx);
@@ -400,7 +537,8 @@ template <typename Ti, typename To>
 void launch_copy_scale(helm_op* op, int l, int nrhs, const Ti* in, To* out, const double* scale,
                        const int* kact, int j) {
   const long long N = op->lev[l].N;
-  dim3 grid(blas_blocks(N, nrhs), nrhs);
+  if (!op->nact) return;
+  dim3 grid(blas_blocks(N, op->nact), op->nact);
   prof_begin(KC_COPY, op->st, l);
   k_copy_scale<Ti, To><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, in, out, scale, K1, kact, j, op->active_d);
   CKL();
@@ -410,7 +548,8 @@ void launch_copy_scale(helm_op* op, int l, int nrhs, const Ti* in, To* out, cons
 template <typename R>
 void launch_restrict(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* out) {
   const LevelDev &F = op->lev[l], &Cc = op->lev[l + 1];
-  dim3 grid(blas_blocks(Cc.N, nrhs), nrhs);
+  if (!op->nact) return;
+  dim3 grid(blas_blocks(Cc.N, op->nact), op->nact);
   const R fac = (R)std::ldexp(1.0, -op->dim);
   prof_begin(KC_RESTRICT, op->st, l);
   k_restrict<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3, fac,
@@ -422,7 +561,8 @@ void launch_restrict(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* out) 
 template <typename R>
 void launch_prolong_add(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* out) {
   const LevelDev &F = op->lev[l], &Cc = op->lev[l + 1];
-  dim3 grid(blas_blocks(F.N, nrhs), nrhs);
+  if (!op->nact) return;
+  dim3 grid(blas_blocks(F.N, op->nact), op->nact);
   prof_begin(KC_PROLONG, op->st, l);
   k_prolong_add<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3,
                                                           in, out, op->active_d);
@@ -517,26 +657,30 @@ void build_tables(helm_op* op) {
     const int Ns[3] = {Lv.nx, Lv.ny, Lv.nz};
     for (int a = 0; a < 3; ++a) {
       const int N = Ns[a];
+      const int NT = N * op->nop;   // op-major: operator o's table at o * N
       if (a == 1 && op->dim == 2) {   // 2D: no y term (tables identically zero)
         for (int adj = 0; adj < 2; ++adj)
-          for (int t = 0; t < 3; ++t) CK(cudaMemsetAsync(Lv.t64[adj][a][t], 0, sizeof(double2) * N, op->st));
+          for (int t = 0; t < 3; ++t) CK(cudaMemsetAsync(Lv.t64[adj][a][t], 0, sizeof(double2) * NT, op->st));
       } else {
-        AxisPml ap{};
-        ap.N = N; ap.n_int = (int)G.n[a]; ap.wlo = G.pml[a][0]; ap.whi = G.pml[a][1]; ap.level = l;
-        ap.h0 = G.h; ap.omega = op->omega; ap.R = op->pml.R; ap.power = op->pml.power; ap.vref = op->vref;
-        prof_count(KC_SETUP);
-        k_tables<<<(N + 127) / 128, 128, 0, op->st>>>(ap, Lv.t64[0][a][0], Lv.t64[0][a][1], Lv.t64[0][a][2]);
-        CKL();
-        prof_count(KC_SETUP);
-        k_tables_adj<<<(N + 127) / 128, 128, 0, op->st>>>(N, Lv.t64[0][a][0], Lv.t64[0][a][1], Lv.t64[0][a][2],
-                                                          Lv.t64[1][a][0], Lv.t64[1][a][1], Lv.t64[1][a][2]);
-        CKL();
+        for (int o = 0; o < op->nop; ++o) {
+          AxisPml ap{};
+          ap.N = N; ap.n_int = (int)G.n[a]; ap.wlo = G.pml[a][0]; ap.whi = G.pml[a][1]; ap.level = l;
+          ap.h0 = G.h; ap.omega = op->omegas[o]; ap.R = op->pml.R; ap.power = op->pml.power; ap.vref = op->vref;
+          double2* T0[3] = {Lv.t64[0][a][0] + (size_t)o * N, Lv.t64[0][a][1] + (size_t)o * N, Lv.t64[0][a][2] + (size_t)o * N};
+          double2* T1[3] = {Lv.t64[1][a][0] + (size_t)o * N, Lv.t64[1][a][1] + (size_t)o * N, Lv.t64[1][a][2] + (size_t)o * N};
+          prof_count(KC_SETUP);
+          k_tables<<<(N + 127) / 128, 128, 0, op->st>>>(ap, T0[0], T0[1], T0[2]);
+          CKL();
+          prof_count(KC_SETUP);
+          k_tables_adj<<<(N + 127) / 128, 128, 0, op->st>>>(N, T0[0], T0[1], T0[2], T1[0], T1[1], T1[2]);
+          CKL();
+        }
       }
       if (op->dtype == HELM_C64)
         for (int adj = 0; adj < 2; ++adj)
           for (int t = 0; t < 3; ++t) {
             prof_count(KC_SETUP);
-            k_cast_c<<<(N + 127) / 128, 128, 0, op->st>>>(N, Lv.t64[adj][a][t], Lv.t32[adj][a][t]);
+            k_cast_c<<<(NT + 127) / 128, 128, 0, op->st>>>(NT, Lv.t64[adj][a][t], Lv.t32[adj][a][t]);
             CKL();
           }
     }
@@ -622,9 +766,19 @@ void op_set_model(helm_op* op, const double* m_host) {
   build_models(op);
 }
 
-void op_set_omega(helm_op* op, double omega) {
-  op->omega = omega;
+void op_set_omegas(helm_op* op, const double* w, int n) {
+  REQ(n >= 1 && n <= HELM_MAXOP, HELM_ERR_ARG, "too many operators in one batch");
+  for (int o = 0; o < n; ++o) REQ(w[o] > 0 && std::isfinite(w[o]), HELM_ERR_ARG, "omega must be > 0");
+  op->nop = n;
+  for (int o = 0; o < n; ++o) op->omegas[o] = w[o];
+  op->omega = w[0];
   build_tables(op);
+}
+void op_set_omega(helm_op* op, double omega) { op_set_omegas(op, &omega, 1); }
+
+// RHS -> operator map of the next solves (joint (source, frequency) batches).
+void op_set_rop(helm_op* op, const std::vector<int>& rop) {
+  CK(cudaMemcpyAsync(op->rop_d, rop.data(), sizeof(int) * rop.size(), cudaMemcpyHostToDevice, op->st));
 }
 
 helm_op* op_create(const helm_grid* grid, const double* m, double omega, const helm_pml* pml, helm_dtype dtype,
@@ -684,8 +838,8 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
     for (int adj = 0; adj < 2; ++adj)
       for (int a = 0; a < 3; ++a)
         for (int t = 0; t < 3; ++t) {
-          Lv.t64[adj][a][t] = dalloc<double2>(op->allocs, Ns[a]);
-          if (dtype == HELM_C64) Lv.t32[adj][a][t] = dalloc<float2>(op->allocs, Ns[a]);
+          Lv.t64[adj][a][t] = dalloc<double2>(op->allocs, (size_t)Ns[a] * HELM_MAXOP);
+          if (dtype == HELM_C64) Lv.t32[adj][a][t] = dalloc<float2>(op->allocs, (size_t)Ns[a] * HELM_MAXOP);
         }
   }
   op->m_int_d = dalloc<double>(op->allocs, n_int);
@@ -699,6 +853,8 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
   op->rb.ticket = dalloc<unsigned>(op->allocs, max_rhs);
   CK(cudaMemset(op->rb.ticket, 0, sizeof(unsigned) * max_rhs));
   op->active_d = dalloc<int>(op->allocs, max_rhs);
+  op->rop_d = dalloc<int>(op->allocs, max_rhs);
+  CK(cudaMemset(op->rop_d, 0, sizeof(int) * max_rhs));
   op->apply_only = apply_only;
   if (apply_only) {
     op->act_h.assign(max_rhs, 1);
@@ -739,8 +895,15 @@ void reset_acct(helm_op* op, int nrhs) {
   std::fill(op->act_h.begin(), op->act_h.begin() + nrhs, 1);
 }
 
+// Upload the compact list of active RHS: kernels launch over these only, so RHS that have
+// converged (or were never active) cost nothing and the whole GPU works on the rest.
 void set_active(helm_op* op, int nrhs) {
-  CK(cudaMemcpyAsync(op->active_d, op->act_h.data(), sizeof(int) * nrhs, cudaMemcpyHostToDevice, op->st));
+  op->alist_h.clear();
+  for (int r = 0; r < nrhs; ++r)
+    if (op->act_h[r]) op->alist_h.push_back(r);
+  op->nact = (int)op->alist_h.size();
+  if (op->nact)
+    CK(cudaMemcpyAsync(op->active_d, op->alist_h.data(), sizeof(int) * op->nact, cudaMemcpyHostToDevice, op->st));
 }
 
 // ------------------------------------------------------------------------------ solve
@@ -880,6 +1043,11 @@ std::vector<long long> to_ext(const helm_grid& G, const int64_t* ids, int n) {
   return e;
 }
 
+// Listing 1 `case OBJ` / FORW_MODEL over this rank's (frequency, source) pairs. The pairs
+// are processed in joint batches of up to max_rhs right-hand sides (frequency-major order):
+// each batch is ONE batched forward solve and ONE batched adjoint solve whose RHS may use
+// different frequencies (per-RHS operator tables, Geo::rop) — the paper's data parallelism
+// over the joint (source, frequency) index set (Fig. 2) inside one GPU.
 template <typename R>
 void fwi_run(helm_op* op, const helm_grid& G, int nfreq, const double* freq, const double* sw, int nsrc_total,
              int s_begin, int s_end, const int64_t* src, int nrec, const int64_t* rec, const double* dobs,
@@ -900,65 +1068,89 @@ void fwi_run(helm_op* op, const helm_grid& G, int nfreq, const double* freq, con
     CK(cudaMemsetAsync(fb.f, 0, sizeof(double), st));
   }
   fb.d = dalloc<double2>(fb.keep, (size_t)B * std::max(nrec, 1));
+  double2* amp_d = dalloc<double2>(fb.keep, B);
+  double* w2_d = dalloc<double>(fb.keep, B);
+  long long* srcb_d = dalloc<long long>(fb.keep, B);
   std::vector<long long> sext = to_ext(G, src + s_begin, ns), rext = to_ext(G, rec, nrec);
   {
     std::vector<long long> sr = rext;
     std::sort(sr.begin(), sr.end());
     REQ(std::adjacent_find(sr.begin(), sr.end()) == sr.end(), HELM_ERR_ARG, "receivers must be distinct nodes");
   }
-  fb.src_ext = dalloc<long long>(fb.keep, std::max(ns, 1));
   fb.rec_ext = dalloc<long long>(fb.keep, std::max(nrec, 1));
-  CK(cudaMemcpyAsync(fb.src_ext, sext.data(), sizeof(long long) * ns, cudaMemcpyHostToDevice, st));
   if (nrec) CK(cudaMemcpyAsync(fb.rec_ext, rext.data(), sizeof(long long) * nrec, cudaMemcpyHostToDevice, st));
   const double hd = std::pow(G.h, (double)G.ndim);
   std::vector<helm_solve_report> rtmp(B);
-  for (int fi = 0; fi < nfreq; ++fi) {
-    const double w = 2.0 * M_PI * freq[fi];
-    if (fi > 0 || op->omega != w) op_set_omega(op, w);
-    const double2 S = sw ? make_double2(sw[2 * fi], sw[2 * fi + 1]) : make_double2(1.0, 0.0);
-    const double2 amp = make_double2(S.x / hd, S.y / hd);
-    for (int s0 = 0; s0 < ns; s0 += B) {
-      const int nb = std::min(B, ns - s0);
-      // a7: inject q_s = S e_s / h^d
-      CK(cudaMemsetAsync(fb.Bq, 0, sizeof(C) * N * nb, st));
-      prof_count(KC_FWI);
-      k_inject<R><<<(nb + 127) / 128, 128, 0, st>>>(nb, N, fb.src_ext + s0, amp, (C*)fb.Bq);
-      CKL();
-      // forward solves u = H^-1 q
-      solve_any(op, 0, nb, fb.Bq, fb.U, so, rtmp.data());
-      for (int b = 0; b < nb; ++b)
-        if (rep) rep[((size_t)fi * ns + s0 + b) * 2 + 0] = rtmp[b];
-      if (d_out) {   // FORW_MODEL: d = P_r u
-        if (nrec) {
-          prof_count(KC_FWI);
-          k_gather_data<R><<<(unsigned)((nb * (long long)nrec + 255) / 256), 256, 0, st>>>(nb, nrec, N, fb.rec_ext,
-                                                                                      (const C*)fb.U, fb.d);
-          CKL();
-          CK(cudaMemcpyAsync(d_out + 2 * (((size_t)fi * ns + s0) * nrec), fb.d, sizeof(double2) * nb * nrec,
-                             cudaMemcpyDeviceToHost, st));
-          CK(cudaStreamSynchronize(st));
-        }
-        continue;
-      }
-      // a7: r = P_r u - d, f += 1/2 |r|^2, adjoint source -P_r^T r
-      CK(cudaMemcpyAsync(fb.d, dobs + 2 * (((size_t)fi * nsrc_total + s_begin + s0) * nrec),
-                         sizeof(double2) * nb * nrec, cudaMemcpyHostToDevice, st));
-      CK(cudaMemsetAsync(fb.A, 0, sizeof(C) * N * nb, st));
-      dim3 gg(std::max(1, std::min(TARGET_BLOCKS, (nb * nrec + 255) / 256)));
-      prof_count(KC_FWI);
-      k_gather_residual<R><<<gg, HELM_RED_THREADS, 0, st>>>(nb, nrec, N, fb.rec_ext, fb.d, (const C*)fb.U, (C*)fb.A,
-                                                              fb.f, op->rb);
-      CKL();
-      // a8: adjoint solves v = H^-H(-P_r^T r)
-      solve_any(op, 1, nb, fb.A, fb.V, so, rtmp.data());
-      for (int b = 0; b < nb; ++b)
-        if (rep) rep[((size_t)fi * ns + s0 + b) * 2 + 1] = rtmp[b];
-      // a9: g_ext += Re(w^2 conj(u) v)
-      prof_count(KC_FWI);
-      k_grad<R><<<blas_blocks(N, 1), 256, 0, st>>>(nb, N, w * w, (const C*)fb.U, (const C*)fb.V, fb.gext);
-      CKL();
+  std::vector<double2> amp_h(B), dbat((size_t)B * std::max(nrec, 1));
+  std::vector<double> w2_h(B), wop;
+  std::vector<long long> srcb_h(B);
+  std::vector<int> rop_h(B), fi_h(B), si_h(B);
+  const long long npairs = (long long)nfreq * ns;
+  for (long long p0 = 0; p0 < npairs; p0 += B) {
+    const int nb = (int)std::min<long long>(B, npairs - p0);
+    // the batch's operators (distinct frequencies, in order) and per-RHS data
+    wop.clear();
+    int last_f = -1;
+    for (int b = 0; b < nb; ++b) {
+      const int fi = (int)((p0 + b) / ns), si = (int)((p0 + b) % ns);
+      if (fi != last_f) { wop.push_back(2.0 * M_PI * freq[fi]); last_f = fi; }
+      fi_h[b] = fi; si_h[b] = si; rop_h[b] = (int)wop.size() - 1;
+      const double2 S = sw ? make_double2(sw[2 * fi], sw[2 * fi + 1]) : make_double2(1.0, 0.0);
+      amp_h[b] = make_double2(S.x / hd, S.y / hd);
+      w2_h[b] = wop.back() * wop.back();
+      srcb_h[b] = sext[si];
     }
+    REQ((int)wop.size() <= HELM_MAXOP, HELM_ERR_ARG, "more than HELM_MAXOP frequencies in one batch");
+    op_set_omegas(op, wop.data(), (int)wop.size());
+    op_set_rop(op, rop_h);
+    CK(cudaMemcpyAsync(amp_d, amp_h.data(), sizeof(double2) * nb, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w2_d, w2_h.data(), sizeof(double) * nb, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(srcb_d, srcb_h.data(), sizeof(long long) * nb, cudaMemcpyHostToDevice, st));
+    // a7: inject q = S(omega) e_s / h^d
+    CK(cudaMemsetAsync(fb.Bq, 0, sizeof(C) * N * nb, st));
+    prof_count(KC_FWI);
+    k_inject<R><<<(nb + 127) / 128, 128, 0, st>>>(nb, N, srcb_d, amp_d, (C*)fb.Bq);
+    CKL();
+    // forward solves u = H^-1 q
+    solve_any(op, 0, nb, fb.Bq, fb.U, so, rtmp.data());
+    for (int b = 0; b < nb; ++b)
+      if (rep) rep[((size_t)fi_h[b] * ns + si_h[b]) * 2 + 0] = rtmp[b];
+    if (d_out) {   // FORW_MODEL: d = P_r u
+      if (nrec) {
+        prof_count(KC_FWI);
+        k_gather_data<R><<<(unsigned)((nb * (long long)nrec + 255) / 256), 256, 0, st>>>(nb, nrec, N, fb.rec_ext,
+                                                                                    (const C*)fb.U, fb.d);
+        CKL();
+        CK(cudaMemcpyAsync(dbat.data(), fb.d, sizeof(double2) * nb * nrec, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int b = 0; b < nb; ++b)
+          std::memcpy(d_out + 2 * (((size_t)fi_h[b] * ns + si_h[b]) * nrec), &dbat[(size_t)b * nrec],
+                      sizeof(double2) * nrec);
+      }
+      continue;
+    }
+    // a7: r = P_r u - d, f += 1/2 |r|^2, adjoint source -P_r^T r
+    for (int b = 0; b < nb; ++b)
+      std::memcpy(&dbat[(size_t)b * nrec], dobs + 2 * (((size_t)fi_h[b] * nsrc_total + s_begin + si_h[b]) * nrec),
+                  sizeof(double2) * nrec);
+    if (nrec) CK(cudaMemcpyAsync(fb.d, dbat.data(), sizeof(double2) * nb * nrec, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(fb.A, 0, sizeof(C) * N * nb, st));
+    dim3 gg(std::max(1, std::min(TARGET_BLOCKS, (nb * nrec + 255) / 256)));
+    prof_count(KC_FWI);
+    k_gather_residual<R><<<gg, HELM_RED_THREADS, 0, st>>>(nb, nrec, N, fb.rec_ext, fb.d, (const C*)fb.U, (C*)fb.A,
+                                                            fb.f, op->rb);
+    CKL();
+    // a8: adjoint solves v = H^-H(-P_r^T r)
+    solve_any(op, 1, nb, fb.A, fb.V, so, rtmp.data());
+    for (int b = 0; b < nb; ++b)
+      if (rep) rep[((size_t)fi_h[b] * ns + si_h[b]) * 2 + 1] = rtmp[b];
+    // a9: g_ext += sum_b Re(omega_b^2 conj(u_b) v_b)
+    prof_count(KC_FWI);
+    k_grad<R><<<blas_blocks(N, 1), 256, 0, st>>>(nb, N, w2_d, (const C*)fb.U, (const C*)fb.V, fb.gext);
+    CKL();
   }
+  // the host staging buffers above are reused across batches: make sure the last copies
+  // are done before they go out of scope
   if (!d_out) {
     const long long nint = G.n[0] * G.n[1] * G.n[2];
     prof_count(KC_FWI);

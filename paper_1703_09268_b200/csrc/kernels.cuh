@@ -5,15 +5,41 @@
 #include "common.cuh"
 
 // ----------------------------------------------------------------------------- geometry
+// One geometry, `nop` operators: the batch of a joint (source, frequency) evaluation
+// (Fig. 2) shares grid and model; operator o = frequency omega_o has its own 1D
+// tables (stored op-major: table o of axis a starts at o * N_a) and omega_o^2. RHS r uses
+// operator rop[r] (rop == null: operator 0).
+#define HELM_MAXOP 16
 template <typename R> struct Geo {
   int nx, ny, nz;          // extended sizes of this level
   long long N;             // nx*ny*nz
   const R* m;              // level model (slowness^2), extended
-  R w2;                    // omega^2
-  const cx<R>* lo[3];      // 1D tables of this operator (H or H^H), axis 0=x,1=y,2=z
+  int nop;                 // operators sharing this geometry
+  const int* rop;          // per-RHS operator index, or null
+  R w2[HELM_MAXOP];        // omega_o^2
+  const cx<R>* lo[3];      // 1D tables (H or H^H), axis 0=x,1=y,2=z, nop tables each
   const cx<R>* dg[3];
   const cx<R>* up[3];
 };
+
+// The 1D tables and omega^2 of RHS r's operator.
+template <typename R> struct OpTab {
+  const cx<R>*lo[3], *dg[3], *up[3];
+  R w2;
+};
+template <typename R> __device__ __forceinline__ OpTab<R> op_tab(const Geo<R>& g, int r) {
+  const int o = g.rop ? g.rop[r] : 0;
+  OpTab<R> t;
+  const long long n[3] = {g.nx, g.ny, g.nz};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    t.lo[a] = g.lo[a] + o * n[a];
+    t.dg[a] = g.dg[a] + o * n[a];
+    t.up[a] = g.up[a] + o * n[a];
+  }
+  t.w2 = g.w2[o];
+  return t;
+}
 
 template <typename R> struct VPtrs { const cx<R>* p[HELM_KMAX + 1]; };
 
@@ -174,8 +200,7 @@ __global__ void k_cast_c(long long n, const double2* __restrict__ a, float2* __r
 template <typename R>
 __global__ void __launch_bounds__(HELM_RED_THREADS)
 k_norm_start(long long N, const cx<R>* __restrict__ b, const int* __restrict__ active, KCtx ctx, RedBuf rb) {
-  const int r = blockIdx.y;
-  if (active && !active[r]) return;
+  const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   const cx<R>* br = b + (long long)r * N;
   double s = 0.0;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
@@ -195,8 +220,7 @@ template <typename Tin, typename Tout>
 __global__ void k_copy_scale(long long N, const Tin* __restrict__ in, Tout* __restrict__ out,
                              const double* __restrict__ scale, int sstride, const int* __restrict__ kact,
                              int jstep, const int* __restrict__ active) {
-  const int r = blockIdx.y;
-  if (active && !active[r]) return;
+  const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   const bool dead = kact && jstep >= kact[r];
   const double s = scale ? scale[(long long)r * sstride] : 1.0;
   const long long off = (long long)r * N;
@@ -211,8 +235,7 @@ __global__ void k_copy_scale(long long N, const Tin* __restrict__ in, Tout* __re
 template <typename R>
 __global__ void k_restrict(int fx, int fy, int fz, int cxn, int cyn, int czn, int has_y, R fac,
                            const cx<R>* __restrict__ in, cx<R>* __restrict__ out, const int* __restrict__ active) {
-  const int r = blockIdx.y;
-  if (active && !active[r]) return;
+  const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   const long long Nc = (long long)cxn * cyn * czn, Nf = (long long)fx * fy * fz;
   const cx<R>* fin = in + (long long)r * Nf;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < Nc; p += (long long)gridDim.x * blockDim.x) {
@@ -244,8 +267,7 @@ __global__ void k_restrict(int fx, int fy, int fz, int cxn, int cyn, int czn, in
 template <typename R>
 __global__ void k_prolong_add(int fx, int fy, int fz, int cxn, int cyn, int czn, int has_y,
                               const cx<R>* __restrict__ in, cx<R>* __restrict__ out, const int* __restrict__ active) {
-  const int r = blockIdx.y;
-  if (active && !active[r]) return;
+  const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   const long long Nc = (long long)cxn * cyn * czn, Nf = (long long)fx * fy * fz;
   const cx<R>* cin = in + (long long)r * Nc;
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < Nf; p += (long long)gridDim.x * blockDim.x) {
@@ -276,11 +298,12 @@ __global__ void k_prolong_add(int fx, int fy, int fz, int cxn, int cyn, int czn,
 }
 
 // ================================================================= a7, a9: FWI kernels
-// q_s = S e_node(s) / h^d (D7); B zeroed beforehand.
+// q_s = S(omega_s) e_node(s) / h^d (D7), one amplitude per RHS; B zeroed beforehand.
 template <typename R>
-__global__ void k_inject(int ns, long long N, const long long* __restrict__ src_ext, double2 amp, cx<R>* __restrict__ B) {
+__global__ void k_inject(int ns, long long N, const long long* __restrict__ src_ext, const double2* __restrict__ amp,
+                         cx<R>* __restrict__ B) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < ns) B[(long long)s * N + src_ext[s]] = from_d<cx<R>>(amp);
+  if (s < ns) B[(long long)s * N + src_ext[s]] = from_d<cx<R>>(amp[s]);
 }
 
 // r = P_r u - d (D8, D10); A = -P_r^T r (D11, receivers distinct); f += 1/2 ||r||^2 (fp64,
@@ -318,17 +341,18 @@ __global__ void k_gather_data(int ns, int nrec, long long N, const long long* __
   d[q] = to_d(U[(long long)si * N + rec_ext[k]]);
 }
 
-// g_ext += sum_s Re(omega^2 conj(u_s) v_s) (Eq. 8, Listing 1), fp64.
+// g_ext += sum_s Re(omega_s^2 conj(u_s) v_s) (Eq. 8, Listing 1), fp64, fixed
+// RHS order (the batch's RHS may carry different frequencies).
 template <typename R>
-__global__ void k_grad(int ns, long long N, double w2, const cx<R>* __restrict__ U, const cx<R>* __restrict__ V,
-                       double* __restrict__ gext) {
+__global__ void k_grad(int ns, long long N, const double* __restrict__ w2, const cx<R>* __restrict__ U,
+                       const cx<R>* __restrict__ V, double* __restrict__ gext) {
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
     double acc = 0.0;
     for (int s = 0; s < ns; ++s) {
       const double2 u = to_d(U[(long long)s * N + p]), v = to_d(V[(long long)s * N + p]);
-      acc += u.x * v.x + u.y * v.y;
+      acc += w2[s] * (u.x * v.x + u.y * v.y);
     }
-    gext[p] += w2 * acc;
+    gext[p] += acc;
   }
 }
 
@@ -362,8 +386,7 @@ template <typename R, int NV>
 __global__ void __launch_bounds__(HELM_RED_THREADS)
 k_update_t(long long N, VPtrs<R> V, int j, cx<R>* __restrict__ w, const int* __restrict__ active, KCtx ctx,
            RedBuf rb) {
-  const int r = blockIdx.y;
-  if (active && !active[r]) return;
+  const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   if (j >= ctx.kact[r]) return;
   const long long off = (long long)r * N;
   cx<R>* wr = w + off;
@@ -411,8 +434,7 @@ template <typename R, int K>
 __global__ void __launch_bounds__(HELM_RED_THREADS)
 k_solupdate_t(long long N, VPtrs<R> Z, const double* __restrict__ zscale, cx<R>* __restrict__ x, int init,
               const int* __restrict__ active, KCtx ctx) {
-  const int r = blockIdx.y;
-  if (active && !active[r]) return;
+  const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   __shared__ cx<R> yc[K];
   __shared__ int s_k;
   if (threadIdx.x == 0) {

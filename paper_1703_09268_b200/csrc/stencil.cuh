@@ -2,16 +2,19 @@
 //
 // Work decomposition. A "row tile" is BX x BY rows of the extended grid: (x, y) points of
 // one RHS in 3D (YC = true), or 32 x-points of 8 right-hand sides in 2D (YC = false; rows
-// are uncoupled RHS and the plane is one x-row). A unit of work is one (row tile, z plane).
-// The grid is exactly one resident wave: `groups` x `cpg` CTAs, where a group is one RHS
-// (3D) or one 8-RHS row group (2D) and its T*nz units are split into cpg equal contiguous
-// ranges. A CTA walks its range as segments (maximal runs inside one row tile) and streams
-// the planes z0-1 .. z1 of each segment through an S-stage shared-memory ring filled by
-// asynchronous copies (cp.async / LDGSTS; zero-fill implements the Dirichlet ghosts, R7):
-// the tile plus its one-point halo for every halo'd operand, the model m, the per-plane
-// z coefficients of the 1D tables and, per mode, the own-point operands. S-3 planes are in
-// flight while plane z is computed. No wave tail, no per-plane global-latency bubble.
-// PML enters only through the 1D tables (D4-D6).
+// are uncoupled RHS and the plane is one x-row). A work item is one row tile over one
+// z-chunk of zlen planes. The grid is one resident wave: `groups` x `cpg` CTAs, a group
+// being one RHS (3D) or one 8-RHS row group (2D); a group's items, ordered (z-chunk, tile)
+// with the tile fastest, are dealt round-robin to its CTAs, so co-resident CTAs sweep
+// neighbouring tiles at the same depth and their halos meet in L2 (the host picks the chunk
+// count that minimises waves x (planes + 2 halo planes) per item). Each item streams the
+// planes z0-1 .. z1 through an S-stage shared-memory ring filled by asynchronous copies
+// (cp.async / LDGSTS; zero-fill implements the Dirichlet ghosts, R7): the tile plus its
+// one-point halo for every halo'd operand, the model m, the per-plane z coefficients of the
+// 1D tables and, per mode, the own-point operands; S-3 planes are in flight while plane z
+// is computed. In 2D every warp owns its row of each stage and synchronises with the warp
+// barrier only — no CTA-wide barrier on the streaming path. PML enters only through the
+// 1D tables (D4-D6).
 //
 // MODE 0: y = s H x              (s = lazy normalisation of x, per RHS)
 // MODE 1: y = b - H x, ||y||     (starts a Krylov cycle: beta, v0 scale, g, kact)
@@ -45,6 +48,12 @@ __device__ __forceinline__ void cpa_wait_n(int n) {
   }
 }
 
+// 3D tiles couple the rows (y) of a CTA: block barrier. 2D rows are independent right-hand
+// sides and each warp owns its row of every ring stage: warp barrier only.
+template <bool YC> __device__ __forceinline__ void csync() {
+  if constexpr (YC) __syncthreads(); else __syncwarp();
+}
+
 template <typename R> struct PlaneArgs {
   Geo<R> g;
   const cx<R>* x;          // halo'd input: x (MODE 0-2); V_0 (MODE 3, NV = 0) or raw W (MODE 3, NV > 0)
@@ -54,12 +63,13 @@ template <typename R> struct PlaneArgs {
   cx<R>* vout;             // MODE 3 (NV > 0): the formed V_NV is written here
   const double* xscale;    // MODE 0/2: per-RHS lazy scale of x (stride sstride) or null
   int sstride;
-  const int* active;       // per-RHS outer mask or null
+  const int* active;       // compact list of the active RHS (null: all); one group each
   const int* kact;         // skip RHS r if jskip >= kact[r] (null = never)
   int jskip;
   int jstep;               // Hessenberg column written (MODE 2, 3)
   int nrhs, ntx, nty;      // row tiles: ntx x nty per group (nty = 1 in 2D)
   int cpg;                 // CTAs per group
+  int nzc, zlen;           // z-chunks per tile and their length
   int S;                   // ring stages (>= 4)
   KCtx ctx;
   RedBuf rb;
@@ -74,7 +84,8 @@ struct PlaneSmem {
   static constexpr size_t m_off = (size_t)NX * XE * sizeof(cx<R>);
   static constexpr size_t p_off = m_off + PE * sizeof(R);
   static constexpr size_t z_off = p_off + (size_t)NP * PE * sizeof(cx<R>);
-  static constexpr size_t stage_bytes = (z_off + 3 * sizeof(cx<R>) + 127) / 128 * 128;
+  static constexpr int ZR = YC ? 1 : BY;               // z-coefficient triples (2D: one per warp)
+  static constexpr size_t stage_bytes = (z_off + ZR * 3 * sizeof(cx<R>) + 127) / 128 * 128;
 };
 
 // MODE 4 = MODE 3 for the LAST step of a cycle: Y = H V_NV is not stored, and ||Y||^2 is
@@ -134,6 +145,41 @@ __device__ __forceinline__ bool warp_slot_reduce(double2 (&v)[NV], double2* part
   return true;
 }
 
+// Per-RHS epilogue of the stencil modes, run by one lane of the last-arriving warp with the
+// reduced totals: MODE 1 starts a Krylov cycle (beta = ||r||); MODE 2 stores projection
+// column jstep; MODE 3/4 finalise column NV-1 with h_{NV,NV-1} = ||V_NV|| (D14 guard), store
+// column NV and, for the last step, close it by Pythagoras.
+template <int MODE, int NV, int NVR>
+__device__ inline void plane_epilogue(const KCtx& ctx, int r, int jstep, const double2 (&tot)[NVR]) {
+  const int K1 = HELM_KMAX + 1;
+  constexpr bool LAST = MODE == 4;
+  if constexpr (MODE == 1) {
+    start_cycle(ctx, r, sqrt(tot[0].x));
+  } else if constexpr (MODE == 2) {
+    const double* scl = ctx.scale + r * K1;
+    double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
+    for (int i = 0; i < NV; ++i) H[hidx(i, jstep)] = make_double2(tot[i].x * scl[i], tot[i].y * scl[i]);
+  } else if constexpr (MODE >= 3) {
+    if constexpr (NV > 0) finalize_column(ctx, r, NV - 1, sqrt(tot[NV + 1].x));
+    const double* scl = ctx.scale + r * K1;
+    const double sj = scl[NV];
+    double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
+    double hh = 0.0;
+    for (int i = 0; i <= NV; ++i) {
+      const double f = scl[i] * sj;
+      const double2 h = make_double2(tot[i].x * f, tot[i].y * f);
+      H[hidx(i, NV)] = h;
+      hh += cabs2(h);
+    }
+    if constexpr (LAST) {
+      if (NV < ctx.kact[r]) {   // column NV is live (no breakdown above)
+        const double w2 = sj * sj * tot[NV + 2].x;
+        finalize_column(ctx, r, NV, sqrt(fmax(w2 - hh, 0.0)));
+      }
+    }
+  }
+}
+
 template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC>
 __global__ void __launch_bounds__(BX * BY / PY)
 k_plane(const PlaneArgs<R> a) {
@@ -160,26 +206,19 @@ k_plane(const PlaneArgs<R> a) {
   const long long plane = YC ? (long long)nx * ny : (long long)nx;
   const C zero = mkc((R)0, (R)0);
 
-  // ---- rows of this thread: its RHS (3D: the group; 2D: group*BY + row)
+  // ---- this CTA's RHS: entry grp of the compact active list
+  static_assert(YC, "2D grids use the register march (march2d.cuh)");
   int rhs[PY];
-  bool ract = true;      // this thread's RHS exists and is active (warp-uniform in 2D)
-  R sc = (R)1;           // lazy scale of x for this thread's RHS (MODE 0 / 2)
-  if constexpr (YC) {
-    const int r = grp;
-    if (a.active && !a.active[r]) return;
+  const bool ract = true;
+  R sc = (R)1;           // lazy scale of x for this RHS (MODE 0 / 2)
+  {
+    const int r = a.active ? a.active[grp] : grp;
     if (a.kact && a.jskip >= a.kact[r]) return;
 #pragma unroll
     for (int k = 0; k < PY; ++k) rhs[k] = r;
-  } else {
-    const int r = grp * BY + ty0;
-    bool ok = r < a.nrhs;
-    if (ok && a.active && !a.active[r]) ok = false;
-    if (ok && a.kact && a.jskip >= a.kact[r]) ok = false;
-    ract = ok;
-    rhs[0] = ok ? r : 0;
-    if (!__syncthreads_or(ract ? 1 : 0)) return;
   }
   if ((MODE == 0 || MODE == 2) && a.xscale && ract) sc = (R)a.xscale[(long long)rhs[0] * a.sstride];
+  const OpTab<R> T = op_tab(g, rhs[0]);
 
   // ---- MODE 3 forming coefficients of this thread's RHS: V_NV = cw W + sum_i cv_i V_i
   R cw = (R)1;
@@ -202,16 +241,14 @@ k_plane(const PlaneArgs<R> a) {
   for (int k = 0; k < NVR; ++k) acc[k] = make_double2(0.0, 0.0);
   double nrm = 0.0, ynrm = 0.0;
 
-  const long long T = (long long)a.ntx * a.nty;
-  const long long U = T * nz;
-  long long u = (U * cig) / a.cpg;
-  const long long u1 = (U * (cig + 1)) / a.cpg;
-
-  while (u < u1) {
-    const int tile = (int)(u / nz);
-    const int z0 = (int)(u % nz);
-    const int z1 = (int)min((long long)nz, z0 + (u1 - u));
-    u += z1 - z0;
+  // work items of this group: (z-chunk, tile), tile fastest, dealt round-robin to the
+  // group's CTAs so that co-resident CTAs sweep neighbouring tiles at the same z (their
+  // halos meet in L2)
+  const int ntile = a.ntx * a.nty;
+  const int nitems = ntile * a.nzc;
+  for (int it = cig; it < (ract ? nitems : 0); it += a.cpg) {
+    const int tile = it % ntile, zc = it / ntile;
+    const int z0 = zc * a.zlen, z1 = min(nz, z0 + a.zlen);
     const int txb = tile % a.ntx, tyb = tile / a.ntx;
     const int ix = txb * BX + tx;
 
@@ -257,11 +294,11 @@ k_plane(const PlaneArgs<R> a) {
     const long long mofs0 = YC ? (long long)rowv[0] * nx + ix : (long long)ix;
 
     const int nq = z1 - z0 + 2;
-    auto load = [&](int q) {
+    auto load = [&](int q, int stg) {
       if (q < nq) {
         const int z = z0 - 1 + q;
         const bool zin = z >= 0 && z < nz;
-        const unsigned st = sbase + (unsigned)((q % S) * SM::stage_bytes);
+        const unsigned st = sbase + (unsigned)(stg * SM::stage_bytes);
         const long long zo = (long long)z * plane;
 #pragma unroll
         for (int t = 0; t < NX; ++t) {
@@ -274,10 +311,11 @@ k_plane(const PlaneArgs<R> a) {
             }
         }
         if (q >= 1 && z < z1) {
-          if (threadIdx.x < 3) {   // z coefficients of plane z: lo, dg, up (ghosts masked, R7)
-            const C* tz = threadIdx.x == 0 ? g.lo[2] : (threadIdx.x == 1 ? g.dg[2] : g.up[2]);
-            const bool p = threadIdx.x == 1 || (threadIdx.x == 0 ? z > 0 : z < nz - 1);
-            cpa<sizeof(C)>(st + (unsigned)(SM::z_off + threadIdx.x * sizeof(C)), p ? tz + z : tz, p);
+          if ((YC ? threadIdx.x : tx) < 3) {   // z coefficients of plane z: lo, dg, up (ghosts masked, R7)
+            const int c3 = YC ? threadIdx.x : tx;
+            const C* tz = c3 == 0 ? T.lo[2] : (c3 == 1 ? T.dg[2] : T.up[2]);
+            const bool p = c3 == 1 || (c3 == 0 ? z > 0 : z < nz - 1);
+            cpa<sizeof(C)>(st + (unsigned)(SM::z_off + ((YC ? 0 : ty0) * 3 + c3) * sizeof(C)), p ? tz + z : tz, p);
           }
 #pragma unroll
           for (int k = 0; k < PY; ++k)
@@ -296,9 +334,9 @@ k_plane(const PlaneArgs<R> a) {
       cpa_commit();   // always commit (possibly empty) so group counting stays uniform
     };
     // MODE 3: turn the raw W tile of stage `q` into V_NV in place (halo included)
-    auto form = [&](int q) {
+    auto form = [&](int stg) {
       if constexpr (FORM) {
-        C* X = reinterpret_cast<C*>(smem + (q % S) * SM::stage_bytes);
+        C* X = reinterpret_cast<C*>(smem + stg * SM::stage_bytes);
         auto f1 = [&](int e) {
           C v = cscale(X[e], cw);
 #pragma unroll
@@ -317,41 +355,47 @@ k_plane(const PlaneArgs<R> a) {
     };
 
     // per-thread operator coefficients along x (and y in 3D)
-    const C lox = (ix > 0 && ix < nx) ? g.lo[0][ix] : zero;
-    const C upx = (ix < nx - 1) ? g.up[0][ix] : zero;
-    const C dgx = ix < nx ? g.dg[0][ix] : zero;
+    const C lox = (ix > 0 && ix < nx) ? T.lo[0][ix] : zero;
+    const C upx = (ix < nx - 1) ? T.up[0][ix] : zero;
+    const C dgx = ix < nx ? T.dg[0][ix] : zero;
     C loy[PY], upy[PY], dgy[PY];
 #pragma unroll
     for (int k = 0; k < PY; ++k) {
       if constexpr (YC) {
         const int iy = rowv[k];
-        loy[k] = (iy > 0 && iy < ny) ? g.lo[1][iy] : zero;
-        upy[k] = (iy < ny - 1) ? g.up[1][iy] : zero;
-        dgy[k] = iy < ny ? g.dg[1][iy] : zero;
+        loy[k] = (iy > 0 && iy < ny) ? T.lo[1][iy] : zero;
+        upy[k] = (iy < ny - 1) ? T.up[1][iy] : zero;
+        dgy[k] = iy < ny ? T.dg[1][iy] : zero;
       } else {
         loy[k] = upy[k] = dgy[k] = zero;
       }
     }
 
-    for (int q = 0; q < S - 1; ++q) load(q);
+    // ring stages are tracked incrementally (no division on the streaming path)
+    auto inc = [S](int x) { return x + 1 == S ? 0 : x + 1; };
+    int s_ld = 0;
+    for (int q = 0; q < S - 1; ++q) { load(q, s_ld); s_ld = inc(s_ld); }
+    int s_m1 = 0;             // stage of plane z-1
     for (int z = z0; z < z1; ++z) {
       const int q = z - z0 + 1;
       cpa_wait_n(S - 4);        // this thread's groups <= q+1 complete (committed: <= q+S-3)
-      __syncthreads();          // ... for every thread; stage (q-2)%S is free again
-      load(q + S - 2);          // S-3 planes in flight while plane z is computed
+      csync<YC>();              // ... for every thread; stage (q-2)%S is free again
+      load(q + S - 2, s_ld);    // S-3 planes in flight while plane z is computed
+      s_ld = inc(s_ld);
+      const int s_0 = inc(s_m1), s_p1 = inc(s_0);
       if constexpr (FORM) {
-        if (z == z0) { form(q - 1); form(q); }
-        form(q + 1);
-        __syncthreads();
+        if (z == z0) { form(s_m1); form(s_0); }
+        form(s_p1);
+        csync<YC>();
       }
-      const unsigned char* st1 = smem + (q % S) * SM::stage_bytes;
-      const C* X0 = reinterpret_cast<const C*>(smem + ((q - 1) % S) * SM::stage_bytes);
+      const unsigned char* st1 = smem + s_0 * SM::stage_bytes;
+      const C* X0 = reinterpret_cast<const C*>(smem + s_m1 * SM::stage_bytes);
       const C* X1 = reinterpret_cast<const C*>(st1);
-      const C* X2 = reinterpret_cast<const C*>(smem + ((q + 1) % S) * SM::stage_bytes);
+      const C* X2 = reinterpret_cast<const C*>(smem + s_p1 * SM::stage_bytes);
       const R* Ms = reinterpret_cast<const R*>(st1 + SM::m_off);
       const C* Ps = reinterpret_cast<const C*>(st1 + SM::p_off);
       const C* Zt = reinterpret_cast<const C*>(st1 + SM::z_off);
-      const C lz = Zt[0], dz = Zt[1], uz = Zt[2];
+      const C lz = Zt[(YC ? 0 : ty0) * 3], dz = Zt[(YC ? 0 : ty0) * 3 + 1], uz = Zt[(YC ? 0 : ty0) * 3 + 2];
       const long long zo = (long long)z * plane;
 #pragma unroll
       for (int k = 0; k < PY; ++k) {
@@ -359,7 +403,7 @@ k_plane(const PlaneArgs<R> a) {
         const int c = (ty0 + k * RS + YH) * XP + tx + 1;
         const int pr = (ty0 + k * RS) * BX + tx;
         const C cur = X1[c];
-        const R wm = g.w2 * Ms[pr];
+        const R wm = T.w2 * Ms[pr];
         // tree-shaped sum: four independent complex products, then two adds
         C t0 = cmul(mkc(dgx.x + dgy[k].x + dz.x + wm, dgx.y + dgy[k].y + dz.y), cur);
         C t1 = cfma(upx, X1[c + 1], cmul(lox, X1[c - 1]));
@@ -392,60 +436,24 @@ k_plane(const PlaneArgs<R> a) {
           }
         }
       }
+      s_m1 = s_0;
     }
     cpa_wait<0>();
-    __syncthreads();   // the next segment's prologue reuses the ring
+    csync<YC>();       // the next item's prologue reuses the ring
   }
 
   if constexpr (MODE != 0) {
     if constexpr (MODE == 1) acc[0] = make_double2(nrm, 0.0);
     if constexpr (MODE >= 3) acc[NV + 1] = make_double2(nrm, 0.0);
     if constexpr (MODE >= 3) acc[NV + 2] = make_double2(ynrm, 0.0);
-    // 3D: every warp of the CTA belongs to RHS grp -> slots (cta in group, warp)
-    // 2D: warp w owns RHS grp*BY + w                -> slots (cta in group)
-    int r, slot, nslots;
-    if constexpr (YC) {
-      r = grp;
-      constexpr int WPB = NT / 32;
-      slot = cig * WPB + (threadIdx.x >> 5);
-      nslots = a.cpg * WPB;
-    } else {
-      r = rhs[0];
-      if (!ract) return;          // warp-uniform: one RHS row per warp
-      slot = cig;
-      nslots = a.cpg;
-    }
+    // every warp of the CTA belongs to RHS rhs[0] -> slots (cta in group, warp)
+    constexpr int WPB = NT / 32;
+    const int r = rhs[0];
+    const int slot = cig * WPB + (threadIdx.x >> 5);
+    const int nslots = a.cpg * WPB;
     double2 tot[NVR];
-    if (warp_slot_reduce<NVR>(acc, a.rb.part + (size_t)r * nslots * NVR, a.rb.ticket + r, slot, nslots, tot)) {
-      if ((threadIdx.x & 31) == 0) {
-        const KCtx& ctx = a.ctx;
-        const int K1 = HELM_KMAX + 1;
-        if constexpr (MODE == 1) {
-          start_cycle(ctx, r, sqrt(tot[0].x));
-        } else if constexpr (MODE == 2) {
-          const double* scl = ctx.scale + r * K1;
-          double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
-          for (int i = 0; i < NV; ++i) H[hidx(i, a.jstep)] = make_double2(tot[i].x * scl[i], tot[i].y * scl[i]);
-        } else {
-          if constexpr (NV > 0) finalize_column(ctx, r, NV - 1, sqrt(tot[NV + 1].x));
-          const double* scl = ctx.scale + r * K1;
-          const double sj = scl[NV];
-          double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
-          double hh = 0.0;
-          for (int i = 0; i <= NV; ++i) {
-            const double f = scl[i] * sj;
-            const double2 h = make_double2(tot[i].x * f, tot[i].y * f);
-            H[hidx(i, NV)] = h;
-            hh += cabs2(h);
-          }
-          if constexpr (LAST) {
-            if (NV < ctx.kact[r]) {   // column NV is live (no breakdown above)
-              const double w2 = sj * sj * tot[NV + 2].x;
-              finalize_column(ctx, r, NV, sqrt(fmax(w2 - hh, 0.0)));
-            }
-          }
-        }
-      }
+    if (warp_slot_reduce<NVR>(acc, a.rb.part + (size_t)grp * nslots * NVR, a.rb.ticket + r, slot, nslots, tot)) {
+      if ((threadIdx.x & 31) == 0) plane_epilogue<MODE, NV>(a.ctx, r, a.jstep, tot);
     }
   }
 }
