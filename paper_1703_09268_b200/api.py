@@ -115,9 +115,10 @@ class HelmOp:
         self.tdtype = TORCH_DTYPE[dtype]
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            L.load().helm_destroy(self._h)
-            self._h = None
+        h = getattr(self, "_h", None)
+        if h and L is not None and L._lib is not None:   # not during interpreter teardown
+            L._lib.helm_destroy(h)
+        self._h = None
 
     @property
     def handle(self):

@@ -53,6 +53,8 @@ struct KCtx {
   double2* sn;     // [nrhs][KMAX]    Givens s (complex)
   double2* g;      // [nrhs][KMAX+1]  rotated rhs beta e1
   int* kact;       // [nrhs]          active Krylov dimension (breakdown / zero rhs)
+  double2* y;      // [nrhs][KMAX]    least-squares solution R y = g of the cycle (set when
+                   //                 its last column closes; zero until then)
   int k;           // inner dimension of this process
 };
 

@@ -219,6 +219,8 @@ KCtx make_ctx(std::vector<void*>& keep, int nrhs, int k) {
   c.sn = dalloc<double2>(keep, (size_t)nrhs * HELM_KMAX);
   c.g = dalloc<double2>(keep, (size_t)nrhs * K1);
   c.kact = dalloc<int>(keep, nrhs);
+  c.y = dalloc<double2>(keep, (size_t)nrhs * HELM_KMAX);
+  CK(cudaMemset(c.y, 0, sizeof(double2) * nrhs * HELM_KMAX));
   c.k = k;
   CK(cudaMemset(c.H, 0, sizeof(double2) * nrhs * K1 * HELM_KMAX));
   CK(cudaMemset(c.kact, 0, sizeof(int) * nrhs));
@@ -327,35 +329,44 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
 }
 
 // 2D: register z-march kernel (march2d.cuh), one warp per (RHS, 30-point strip, z-chunk)
-// item; exactly one resident wave of warps, split evenly over the right-hand sides.
-// Register prefetch depth (planes). Measured on B200 (scripts/tune_plane.py): deeper
-// prefetch of many operands costs occupancy faster than it adds bytes in flight, so the
-// multi-operand modes keep P = 2.
-template <typename R, int MODE, int NV> constexpr int march_p() {
-  if constexpr (MODE == 0) return sizeof(R) == 4 ? 8 : 6;
-  if constexpr (MODE == 1) return sizeof(R) == 4 ? 6 : 4;
-  return NV <= 1 ? 3 : 2;
-}
-
+// item; exactly one resident wave of warps, split evenly over the active right-hand sides.
+// The per-lane cp.async ring holds S planes (S-2 in flight): S is the largest depth <= 16
+// whose rings fit a shared-memory budget of ~220 KB / occ_target CTAs (4 by default, i.e.
+// 16 warps per SM; HELM_MARCH_OCC / HELM_MARCH_S override for tuning).
 template <typename R, int MODE, int NV>
 void run_march(MarchArgs<R>& a, cudaStream_t st) {
-  constexpr int P = march_p<R, MODE, NV>();
-  auto kern = k_march2d<R, MODE, NV, P>;
-  const size_t zs = (size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>);
-  static int occ = 0;
-  static size_t zs_max = 0;
-  if (zs > zs_max) {   // occupancy for the largest z-table seen so far
-    if (zs > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zs));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, zs));
+  auto kern = k_march2d<R, MODE, NV>;
+  constexpr int SB = MarchShape<R, MODE, NV>::stage_bytes;
+  const size_t zbytes = ((size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>) + 15) / 16 * 16;
+  static const int occ_t = std::max(1, env_int("HELM_MARCH_OCC", 4));
+  static const int s_fix = env_int("HELM_MARCH_S", 0);
+  int S = s_fix >= 3 ? s_fix : (int)(((220 * 1024) / occ_t - (long long)zbytes) / (4 * SB));
+  S = std::max(3, std::min(S, 16));
+  const size_t smem = zbytes + (size_t)4 * S * SB;
+  struct Cfg { size_t smem = 0; int occ = 0; };
+  static Cfg cache[4];   // small cache of (smem -> occupancy)
+  static size_t attr_max = 48 * 1024;   // the opt-in limit only ever grows
+  if (smem > attr_max) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_max = smem;
+  }
+  int occ = 0;
+  for (auto& c : cache)
+    if (c.smem == smem) { occ = c.occ; break; }
+  if (!occ) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem));
     if (occ < 1) throw HelmErr{HELM_ERR_STATE, "march kernel does not fit on an SM"};
-    zs_max = zs;
+    static int next = 0;
+    cache[next] = Cfg{smem, occ};
+    next = (next + 1) % 4;
     if (env_int("HELM_DEBUG", 0)) {
       cudaFuncAttributes fa{};
       cudaFuncGetAttributes(&fa, kern);
-      std::fprintf(stderr, "[helm] march2d R=%zu mode=%d nv=%d P=%d regs=%d occ=%d warps/SM=%d\n", sizeof(R), MODE, NV,
-                   P, fa.numRegs, occ, occ * 4);
+      std::fprintf(stderr, "[helm] march2d R=%zu mode=%d nv=%d S=%d smem=%zu regs=%d occ=%d warps/SM=%d\n", sizeof(R),
+                   MODE, NV, S, smem, fa.numRegs, occ, occ * 4);
     }
   }
+  a.S = S;
   const long long W = (long long)num_sms() * occ * 4;
   const int wpr = (int)std::max(1LL, W / a.nrhs);
   const int nz = a.g.nz;
@@ -365,52 +376,13 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
     const int zl = (nz + n - 1) / n, nzc = (nz + zl - 1) / zl;
     if (nzc != n) continue;
     const long long items = (long long)a.nstrip * nzc;
-    const long long cost = ((items + wpr - 1) / wpr) * (zl + 2 + P);
+    const long long cost = ((items + wpr - 1) / wpr) * (zl + 2 + S / 2);
     if (best < 0 || cost < best) { best = cost; nzc_b = nzc; zl_b = zl; }
   }
   a.nzc = nzc_b; a.zlen = zl_b;
   a.wpr = (int)std::min<long long>(wpr, (long long)a.nstrip * nzc_b);
   const long long warps = (long long)a.nrhs * a.wpr;
-  kern<<<(unsigned)((warps + 3) / 4), 128, zs, st>>>(a);
-}
-
-// 3D y = s H x: register z-march with RY y-rows per warp (march2d.cuh k_march3d).
-template <typename R, int RY>
-void run_march3d(March3Args<R>& a, cudaStream_t st) {
-  constexpr int P = (RY >= 4 && sizeof(R) == 8) ? 1 : 2;
-  auto kern = k_march3d<R, RY, P>;
-  const size_t zs = (size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>);
-  static int occ = 0;
-  static size_t zs_max = 0;
-  if (zs > zs_max) {
-    if (zs > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zs));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, zs));
-    if (occ < 1) throw HelmErr{HELM_ERR_STATE, "march3d kernel does not fit on an SM"};
-    zs_max = zs;
-    if (env_int("HELM_DEBUG", 0)) {
-      cudaFuncAttributes fa{};
-      cudaFuncGetAttributes(&fa, kern);
-      std::fprintf(stderr, "[helm] march3d R=%zu RY=%d P=%d regs=%d occ=%d warps/SM=%d\n", sizeof(R), RY, P, fa.numRegs,
-                   occ, occ * 4);
-    }
-  }
-  const long long W = (long long)num_sms() * occ * 4;
-  const int wpr = (int)std::max(1LL, W / a.nrhs);
-  a.nyb = (a.g.ny + RY - 1) / RY;
-  const long long per_z = (long long)a.nyb * a.nstrip;
-  const int nz = a.g.nz;
-  long long best = -1;
-  int nzc_b = 1, zl_b = nz;
-  for (int n = 1; n <= nz; ++n) {
-    const int zl = (nz + n - 1) / n, nzc = (nz + zl - 1) / zl;
-    if (nzc != n) continue;
-    const long long cost = ((per_z * nzc + wpr - 1) / wpr) * (zl + 2 + P);
-    if (best < 0 || cost < best) { best = cost; nzc_b = nzc; zl_b = zl; }
-  }
-  a.nzc = nzc_b; a.zlen = zl_b;
-  a.wpr = (int)std::min<long long>(wpr, per_z * nzc_b);
-  const long long warps = (long long)a.nrhs * a.wpr;
-  kern<<<(unsigned)((warps + 3) / 4), 128, zs, st>>>(a);
+  kern<<<(unsigned)((warps + 3) / 4), 128, smem, st>>>(a);
 }
 
 // Plane-streaming stencil (stencil.cuh). mode 0: y = s H x; 1: y = b - H x (+cycle start);
@@ -445,19 +417,6 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
     else if (mode == 2) dispatch_k(nv, [&](auto c) { run_march<R, 2, decltype(c)::value>(m, op->st); });
     else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_march<R, 3, decltype(c)::value>(m, op->st); });
     else dispatch_k0(nv, [&](auto c) { run_march<R, 4, decltype(c)::value>(m, op->st); });
-    CKL();
-    prof_end(cls, op->st, acct(op, l, per * m.g.N, true, nrhs));
-    return;
-  }
-  static const int mv3d_ry = env_int("HELM_MV3D_RY", 0);
-  if (mode == 0 && mv3d_ry > 0) {   // 3D matvec: register z-march
-    March3Args<R> m{};
-    m.g = geo<R>(op, l, adj);
-    m.x = x; m.y = y; m.xscale = xscale; m.sstride = K1; m.active = op->active_d; m.nrhs = op->nact;
-    m.nstrip = (m.g.nx + 29) / 30;
-    prof_begin(cls, op->st, l);
-    if (mv3d_ry == 2) run_march3d<R, 2>(m, op->st);
-    else run_march3d<R, 4>(m, op->st);
     CKL();
     prof_end(cls, op->st, acct(op, l, per * m.g.N, true, nrhs));
     return;
@@ -1224,7 +1183,7 @@ double probe_run(helm_op* op, int level, int kind, int nv, int nrhs, int reps) {
   KCtx& ctx = sm ? w.ctxS : w.ctxC;
   REQ(V[0] && Wx, HELM_ERR_STATE, "no workspace on this level");
   const int k = sm ? op->ml.ks_i : op->ml.kc_i;
-  REQ(nv >= 0 && nv < k, HELM_ERR_ARG, "nv out of range");
+  REQ(nv >= 0 && (nv < k || (kind == 10 && nv == k)), HELM_ERR_ARG, "nv out of range");
   const long long N = op->lev[level].N;
   for (int i = 0; i <= k; ++i) CK(cudaMemsetAsync(V[i], 0x3f, sizeof(cx<R>) * N * nrhs, op->st));
   CK(cudaMemsetAsync(Wx, 0x3f, sizeof(cx<R>) * N * nrhs, op->st));

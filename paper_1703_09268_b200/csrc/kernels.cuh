@@ -57,6 +57,25 @@ __device__ inline void start_cycle(const KCtx& ctx, int r, double beta) {
   ctx.scale[r * K1] = beta > 0.0 ? 1.0 / beta : 0.0;
   for (int i = 0; i <= HELM_KMAX; ++i) ctx.g[r * K1 + i] = make_double2(i == 0 ? beta : 0.0, 0.0);
   ctx.kact[r] = beta > 0.0 ? ctx.k : 0;
+  for (int i = 0; i < HELM_KMAX; ++i) ctx.y[r * HELM_KMAX + i] = make_double2(0.0, 0.0);
+}
+
+// Back substitution R y = g over the cycle's kact columns (the rotated Hessenberg), once
+// per RHS when the last column closes; the solution update then only reads y.
+__device__ inline void solve_ls(const KCtx& ctx, int r) {
+  constexpr int K1 = HELM_KMAX + 1;
+  const int k = ctx.kact[r];
+  const double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
+  const double2* gv = ctx.g + r * K1;
+  double2 yv[HELM_KMAX];
+  for (int i = HELM_KMAX - 1; i >= 0; --i) {
+    if (i >= k) { yv[i] = make_double2(0.0, 0.0); continue; }
+    double2 t = gv[i];
+    for (int l = i + 1; l < k; ++l) t = csub(t, cmul(H[hidx(i, l)], yv[l]));
+    const double2 d = H[hidx(i, i)];
+    yv[i] = (d.x == 0.0 && d.y == 0.0) ? make_double2(0.0, 0.0) : cdiv(t, d);
+  }
+  for (int i = 0; i < HELM_KMAX; ++i) ctx.y[r * HELM_KMAX + i] = yv[i];
 }
 
 // Column j of the Hessenberg of RHS r is complete once h_{j+1,j} = hn is known: apply the
@@ -94,6 +113,7 @@ __device__ inline void finalize_column(const KCtx& ctx, int r, int j, double hn)
   } else {
     ctx.scale[r * K1 + j + 1] = 1.0 / hn;
   }
+  if (j + 1 >= ctx.kact[r]) solve_ls(ctx, r);        // the cycle's last column closed
 }
 
 // ================================================================= a1: setup (D2-D4, D6, D13)
@@ -437,24 +457,14 @@ k_solupdate_t(long long N, VPtrs<R> Z, const double* __restrict__ zscale, cx<R>*
   const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   __shared__ cx<R> yc[K];
   __shared__ int s_k;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < K) {
     const int K1 = HELM_KMAX + 1;
+    const int i = threadIdx.x;
     const int k = ctx.kact[r];
-    const double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
-    const double2* gv = ctx.g + r * K1;
-    double2 yv[K];
-    for (int i = K - 1; i >= 0; --i) {
-      if (i >= k) { yv[i] = make_double2(0.0, 0.0); continue; }
-      double2 t = gv[i];
-      for (int l = i + 1; l < k; ++l) t = csub(t, cmul(H[hidx(i, l)], yv[l]));
-      const double2 d = H[hidx(i, i)];
-      yv[i] = (d.x == 0.0 && d.y == 0.0) ? make_double2(0.0, 0.0) : cdiv(t, d);
-    }
-    for (int i = 0; i < K; ++i) {
-      const double sc = (zscale && i < k) ? zscale[r * K1 + i] : 1.0;
-      yc[i] = from_d<cx<R>>(make_double2(yv[i].x * sc, yv[i].y * sc));
-    }
-    s_k = k;
+    const double2 yv = ctx.y[r * HELM_KMAX + i];
+    const double sc = (zscale && i < k) ? zscale[r * K1 + i] : 1.0;
+    yc[i] = from_d<cx<R>>(make_double2(yv.x * sc, yv.y * sc));
+    if (i == 0) s_k = k;
   }
   __syncthreads();
   const int k = s_k;

@@ -8,7 +8,7 @@ for spec in "${ARR[@]}"; do
   set -- $spec
   name=${TAG}_$1_L$2_k$3_nv$4
   python scripts/ncu_targets.py probe $spec > gpurun_out/${name}_plain.log 2>&1 &&
-  ncu --set full --clock-control none --import-source on -k regex:k_plane -s 2 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-k_plane} -s 2 -c 1 \
       -o gpurun_out/${name} python scripts/ncu_targets.py probe $spec > gpurun_out/${name}_ncu.log 2>&1
   echo "$name rc=$?"
   if [ -f gpurun_out/${name}.ncu-rep ]; then

@@ -28,7 +28,7 @@ levels = op.levels()
 Sc, Sr = (16, 8) if dt == api.C128 else (8, 4)
 out = {"case": what, "dtype": "c128" if dt == api.C128 else "c64", "env": {k: v for k, v in os.environ.items() if k.startswith("HELM_")},
        "rows": []}
-kinds = [(0, 0, 2), (1, 0, 3), (3, 0, 2), (3, 1, 4), (3, 2, 5), (3, 3, 6), (4, 4, 6), (2, 2, 5), (10, 5, 7), (11, 2, 5), (12, 0, 1)]
+kinds = [(0, 0, 2), (1, 0, 3), (3, 0, 2), (3, 1, 4), (3, 2, 5), (3, 3, 6), (4, 4, 6), (2, 2, 5), (10, 5, 7), (11, 2, 5), (11, 4, 7), (12, 0, 1)]
 for l, (nx, ny, nz) in enumerate(levels):
     N = nx * ny * nz
     for kind, nv, nvec in kinds:

@@ -40,8 +40,9 @@ def cfg2_oracle():
 @pytest.mark.parametrize("dtype", [api.C128, api.C64])
 def test_cfg2_full_evaluation_matches_oracle(cfg2_oracle, dtype):
     p, d, f_ref, g_ref = cfg2_oracle
+    # bench.py's launch configuration: one joint (source, frequency) batch of all 150 pairs
     fg, rep = api.fwi_misfit_grad(api.Grid.of(p), p.m, p.freqs, p.src, p.rec, d, api.Pml(v_ref=VREF2), dtype,
-                                  api.SolveOpts(rtol=1e-6), max_rhs=50)
+                                  api.SolveOpts(rtol=1e-6), max_rhs=150)
     fg = fg.cpu().numpy()
     assert len(rep) == 300 and all(r["converged"] and r["rel_residual"] <= 1e-6 for r in rep)
     assert abs(fg[0] - f_ref) <= 1e-5 * f_ref
