@@ -170,6 +170,7 @@ def run_ours(args, rank, size, dev):
     # every `probe_stride`-th launch bracketed by CUDA events (not part of `value`)
     timed(1, profile=True)
     prof = api.profile_read()
+    prof_lv = {lv: api.profile_read(lv) for lv in range(4)}
     api.profile(False, 1)
     ms_e2e, _, _ = timed(max(1, min(args.steps, 2)), host_roundtrip=True)
     k_e2e = max(1, min(args.steps, 2))
@@ -178,23 +179,42 @@ def run_ours(args, rank, size, dev):
     e2e_value = solves_per_step * size * k_e2e / (ms_e2e / 1e3)
     hbm, peak_kind = peaks()
 
-    # dominant kernel class by estimated share of device time
+    # shares of device time per kernel class, and the dominant (class, level) pair: its live
+    # roofline is algorithmic bytes / event-timed duration over its sampled launches
     est = {}
     for name, p in prof.items():
         if p["sampled"]:
             est[name] = p["ms"] * p["launches"] / p["sampled"]
     total_est = sum(est.values()) or 1.0
-    dom = max(est, key=est.get) if est else None
-    roof = None
-    if dom:
-        p = prof[dom]
-        achieved = p["bytes"] / (p["ms"] / 1e3) / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": traffic_for(dom), "peak_kind": peak_kind,
-                "share_of_step": round(est[dom] / total_est, 3),
-                "avg_launch_us": round(1e3 * p["ms"] / p["sampled"], 2),
-                "alg_bytes_per_launch": round(p["bytes"] / p["sampled"])}
     kernel_shares = {k: round(v / total_est, 3) for k, v in sorted(est.items(), key=lambda kv: -kv[1])}
+    cl = {}
+    for lv, pr in prof_lv.items():
+        for name, p in pr.items():
+            if p["sampled"]:
+                cl[(name, lv)] = p
+    def est_ms(p):
+        return p["ms"] * p["launches"] / p["sampled"]
+    roof = None
+    level_shares = {}
+    for (name, lv), p in cl.items():
+        level_shares.setdefault(f"L{lv}", 0.0)
+        level_shares[f"L{lv}"] += est_ms(p) / total_est
+    level_shares = {k: round(v, 3) for k, v in sorted(level_shares.items())}
+    if cl:
+        (dname, dlv), p = max(cl.items(), key=lambda kv: est_ms(kv[1]))
+        achieved = p["bytes"] / (p["ms"] / 1e3) / 1e9
+        tr = traffic_for(f"{dname}@L{dlv}")
+        roof = {"kernel": f"{dname} (fused GMRES Arnoldi step, k_march2d MODE 3/4) at level {dlv}" if dname == "arnoldi"
+                else f"{dname} at level {dlv}", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                "traffic": round(tr["ratio"] * p["bytes"] / p["sampled"]) if tr else None,
+                "traffic_note": tr.get("note") if tr else None,
+                "peak_kind": peak_kind, "share_of_step": round(est_ms(p) / total_est, 3),
+                "avg_launch_us": round(1e3 * p["ms"] / p["sampled"], 2),
+                "alg_bytes_per_launch": round(p["bytes"] / p["sampled"]), "sampled_launches": p["sampled"]}
+        cls_all = prof[dname]
+        roof["class_all_levels"] = {"achieved": round(cls_all["bytes"] / (cls_all["ms"] / 1e3) / 1e9, 1),
+                                    "share_of_step": kernel_shares.get(dname)}
 
     cycles = [r["outer_cycles"] for r in (reps or [])]
     # whole-step algorithmic HBM bytes counted by the library (every executed kernel, SURVEY d.2)
@@ -220,6 +240,7 @@ def run_ours(args, rank, size, dev):
         "gpu_launches": int(launches),
         "roofline": roof,
         "kernel_shares": kernel_shares,
+        "level_shares": level_shares,
         "solve_roofline": solve_roof,
         "clocks": clk.summary(),
     }
@@ -231,12 +252,14 @@ def ws_bytes(grid, dtype, max_rhs):
     return 24 * grid.n_ext * max_rhs * sc
 
 
-def traffic_for(kernel):
-    """dram bytes per launch from the committed ncu --set full capture, if any."""
+def traffic_for(key):
+    """DRAM traffic / algorithmic bytes of a (class, level) pair from the committed ncu --set full
+    capture (profiles/ncu_traffic.json, written from the capture's dram__bytes_read.sum +
+    dram__bytes_write.sum of the same kernels), or None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(kernel)
+            return json.load(f).get(key)
     except Exception:
         return None
 

@@ -9,6 +9,10 @@ import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "lib", "libhelm.so")
+# A/B tuning only: HELM_LIB_VARIANT=name loads lib/libhelm_<name>.so (an in-tree build of
+# another revision of the same C ABI)
+if os.environ.get("HELM_LIB_VARIANT"):
+    LIB_PATH = os.path.join(_PKG, "lib", "libhelm_%s.so" % os.environ["HELM_LIB_VARIANT"])
 
 
 class HelmGrid(C.Structure):

@@ -60,6 +60,14 @@ struct KCtx {
 
 __device__ __forceinline__ int hidx(int i, int j) { return i * HELM_KMAX + j; }
 
+// Programmatic dependent launch (sm_90+): the hot-path kernels are launched so that the next
+// kernel's launch and block scheduling overlap this one's tail. Every such kernel calls
+// pdl_wait() before touching memory (it returns once the preceding grid has completed and
+// flushed) and pdl_trigger() to let its dependent launch early. Both are no-ops for a
+// normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // ---------------------------------------------------------------- deterministic reductions
 // Block-wide sum of NV fp64 complex values; fixed shuffle + fixed smem order (no atomics on
 // data), result valid in thread 0.

@@ -133,6 +133,8 @@ struct LevelDev {
   float* m32 = nullptr;
   double2* t64[2][3][3] = {};   // [adjoint][axis][lo,dg,up]
   float2* t32[2][3][3] = {};
+  double2* z64[2] = {};         // packed z coefficients per adjoint (k_zpack)
+  float2* z32[2] = {};
   int tiles = 0;
 };
 
@@ -235,6 +237,7 @@ template <> Geo<double> geo<double>(const helm_op* op, int l, int adj) {
   g.m = L.m64; g.nop = op->nop; g.rop = op->nop > 1 ? op->rop_d : nullptr;
   for (int o = 0; o < op->nop; ++o) g.w2[o] = op->omegas[o] * op->omegas[o];
   for (int a = 0; a < 3; ++a) { g.lo[a] = L.t64[adj][a][0]; g.dg[a] = L.t64[adj][a][1]; g.up[a] = L.t64[adj][a][2]; }
+  g.zpk = L.z64[adj];
   return g;
 }
 template <> Geo<float> geo<float>(const helm_op* op, int l, int adj) {
@@ -244,6 +247,7 @@ template <> Geo<float> geo<float>(const helm_op* op, int l, int adj) {
   g.m = L.m32; g.nop = op->nop; g.rop = op->nop > 1 ? op->rop_d : nullptr;
   for (int o = 0; o < op->nop; ++o) g.w2[o] = (float)(op->omegas[o] * op->omegas[o]);
   for (int a = 0; a < 3; ++a) { g.lo[a] = L.t32[adj][a][0]; g.dg[a] = L.t32[adj][a][1]; g.up[a] = L.t32[adj][a][2]; }
+  g.zpk = L.z32[adj];
   return g;
 }
 
@@ -255,6 +259,30 @@ template <int N = 1, typename F> void dispatch_k(int k, F&& f) {
   } else {
     throw HelmErr{HELM_ERR_ARG, "Krylov dimension out of range"};
   }
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+// Hot-path launches use programmatic dependent launch (see common.cuh pdl_wait): the
+// launch and block scheduling of each kernel overlap the tail of its predecessor.
+// HELM_PDL=0 disables it (plain stream order).
+template <typename... KArgs, typename... Args>
+void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  static const bool on = env_int("HELM_PDL", 0) != 0;   // measured: slower on B200 here (opt-in)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
 }
 
 template <int N = 0, typename F> void dispatch_k0(int k, F&& f) {
@@ -272,10 +300,6 @@ template <int N = 0, typename F> void dispatch_k0(int k, F&& f) {
 // HELM_PLANE_OCC / HELM_PLANE_S override, for tuning).
 template <int MODE, bool YC> constexpr int plane_py() { return (YC && MODE < 3) ? 2 : 1; }
 
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::atoi(v) : dflt;
-}
 struct PlaneTune { int occ_target, s_fixed; };
 const PlaneTune& plane_tune() {
   static const PlaneTune t{std::max(1, env_int("HELM_PLANE_OCC", 4)), env_int("HELM_PLANE_S", 0)};
@@ -325,7 +349,7 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
   a.cpg = sp.cpg; a.nzc = sp.nzc; a.zlen = sp.zlen;
   a.S = cfg.S;
   const long long cpg = sp.cpg;
-  kern<<<(unsigned)(groups * cpg), NT, cfg.smem, st>>>(a);
+  pdl_launch(kern, dim3((unsigned)(groups * cpg)), dim3(NT), cfg.smem, st, a);
 }
 
 // 2D: register z-march kernel (march2d.cuh), one warp per (RHS, 30-point strip, z-chunk)
@@ -372,7 +396,7 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
   const int nz = a.g.nz;
   long long best = -1;
   int nzc_b = 1, zl_b = nz;
-  for (int n = 1; n <= nz; ++n) {
+  for (int n = 1; n <= nz; ++n) {   // z-chunk count minimising rounds x (chunk + halo + ring fill)
     const int zl = (nz + n - 1) / n, nzc = (nz + zl - 1) / zl;
     if (nzc != n) continue;
     const long long items = (long long)a.nstrip * nzc;
@@ -382,7 +406,7 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
   a.nzc = nzc_b; a.zlen = zl_b;
   a.wpr = (int)std::min<long long>(wpr, (long long)a.nstrip * nzc_b);
   const long long warps = (long long)a.nrhs * a.wpr;
-  kern<<<(unsigned)((warps + 3) / 4), 128, smem, st>>>(a);
+  pdl_launch(kern, dim3((unsigned)((warps + 3) / 4)), dim3(128), smem, st, a);
 }
 
 // Plane-streaming stencil (stencil.cuh). mode 0: y = s H x; 1: y = b - H x (+cycle start);
@@ -460,7 +484,7 @@ void launch_norm_start(helm_op* op, int l, int nrhs, const cx<R>* b, const KCtx&
   if (!op->nact) return;
   dim3 grid(blas_blocks(N, op->nact), op->nact);
   prof_begin(KC_NORM, op->st, l);
-  k_norm_start<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, b, op->active_d, ctx, op->rb);
+  pdl_launch(k_norm_start<R>, grid, dim3(HELM_RED_THREADS), 0, op->st, N, b, (const int*)op->active_d, ctx, op->rb);
   CKL();
   prof_end(KC_NORM, op->st, acct(op, l, sizeof(cx<R>) * (double)N, false, nrhs));
 }
@@ -472,7 +496,8 @@ void launch_update(helm_op* op, int l, int nrhs, const VPtrs<R>& V, int j, cx<R>
   dim3 grid(blas_blocks(N, op->nact), op->nact);
   prof_begin(KC_UPDATE, op->st, l);
   dispatch_k(j + 1, [&](auto c) {
-    k_update_t<R, decltype(c)::value><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, V, j, w, op->active_d, ctx, op->rb);
+    pdl_launch(k_update_t<R, decltype(c)::value>, grid, dim3(HELM_RED_THREADS), 0, op->st, N, V, j, w,
+               (const int*)op->active_d, ctx, op->rb);
   });
   CKL();
   prof_end(KC_UPDATE, op->st, acct(op, l, (j + 3.0) * sizeof(cx<R>) * N, false, nrhs));
@@ -486,7 +511,8 @@ void launch_solupdate(helm_op* op, int l, int nrhs, const VPtrs<R>& Z, const dou
   dim3 grid(blas_blocks(N, op->nact), op->nact);
   prof_begin(KC_SOLUPD, op->st, l);
   dispatch_k(k, [&](auto c) {
-    k_solupdate_t<R, decltype(c)::value><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, Z, zscale, x, init, op->active_d, ctx);
+    pdl_launch(k_solupdate_t<R, decltype(c)::value>, grid, dim3(HELM_RED_THREADS), 0, op->st, N, Z, zscale, x, init,
+               (const int*)op->active_d, ctx);
   });
   CKL();
   prof_end(KC_SOLUPD, op->st, acct(op, l, (k + (init ? 1.0 : 2.0)) * sizeof(cx<R>) * N, false, nrhs));
@@ -499,7 +525,8 @@ void launch_copy_scale(helm_op* op, int l, int nrhs, const Ti* in, To* out, cons
   if (!op->nact) return;
   dim3 grid(blas_blocks(N, op->nact), op->nact);
   prof_begin(KC_COPY, op->st, l);
-  k_copy_scale<Ti, To><<<grid, HELM_RED_THREADS, 0, op->st>>>(N, in, out, scale, K1, kact, j, op->active_d);
+  pdl_launch(k_copy_scale<Ti, To>, grid, dim3(HELM_RED_THREADS), 0, op->st, N, in, out, scale, (int)K1, kact, j,
+             (const int*)op->active_d);
   CKL();
   prof_end(KC_COPY, op->st, acct(op, l, (double)(sizeof(Ti) + sizeof(To)) * N, false, nrhs));
 }
@@ -511,8 +538,8 @@ void launch_restrict(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* out) 
   dim3 grid(blas_blocks(Cc.N, op->nact), op->nact);
   const R fac = (R)std::ldexp(1.0, -op->dim);
   prof_begin(KC_RESTRICT, op->st, l);
-  k_restrict<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3, fac,
-                                                       in, out, op->active_d);
+  pdl_launch(k_restrict<R>, grid, dim3(HELM_RED_THREADS), 0, op->st, F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz,
+             (int)(op->dim == 3), fac, in, out, (const int*)op->active_d);
   CKL();
   prof_end(KC_RESTRICT, op->st, acct(op, l, sizeof(cx<R>) * (double)(F.N + Cc.N), false, nrhs));
 }
@@ -523,8 +550,8 @@ void launch_prolong_add(helm_op* op, int l, int nrhs, const cx<R>* in, cx<R>* ou
   if (!op->nact) return;
   dim3 grid(blas_blocks(F.N, op->nact), op->nact);
   prof_begin(KC_PROLONG, op->st, l);
-  k_prolong_add<R><<<grid, HELM_RED_THREADS, 0, op->st>>>(F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz, op->dim == 3,
-                                                          in, out, op->active_d);
+  pdl_launch(k_prolong_add<R>, grid, dim3(HELM_RED_THREADS), 0, op->st, F.nx, F.ny, F.nz, Cc.nx, Cc.ny, Cc.nz,
+             (int)(op->dim == 3), in, out, (const int*)op->active_d);
   CKL();
   prof_end(KC_PROLONG, op->st, acct(op, l, sizeof(cx<R>) * (double)(2 * F.N + Cc.N), false, nrhs));
 }
@@ -642,6 +669,19 @@ void build_tables(helm_op* op) {
             k_cast_c<<<(NT + 127) / 128, 128, 0, op->st>>>(NT, Lv.t64[adj][a][t], Lv.t32[adj][a][t]);
             CKL();
           }
+    }
+    const int nzo = Lv.nz * op->nop;
+    for (int adj = 0; adj < 2; ++adj) {
+      prof_count(KC_SETUP);
+      k_zpack<double2><<<(nzo + 127) / 128, 128, 0, op->st>>>(Lv.nz, op->nop, Lv.t64[adj][2][0], Lv.t64[adj][2][1],
+                                                              Lv.t64[adj][2][2], Lv.z64[adj]);
+      CKL();
+      if (op->dtype == HELM_C64) {
+        prof_count(KC_SETUP);
+        k_zpack<float2><<<(nzo + 127) / 128, 128, 0, op->st>>>(Lv.nz, op->nop, Lv.t32[adj][2][0], Lv.t32[adj][2][1],
+                                                               Lv.t32[adj][2][2], Lv.z32[adj]);
+        CKL();
+      }
     }
   }
 }
@@ -800,6 +840,10 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
           Lv.t64[adj][a][t] = dalloc<double2>(op->allocs, (size_t)Ns[a] * HELM_MAXOP);
           if (dtype == HELM_C64) Lv.t32[adj][a][t] = dalloc<float2>(op->allocs, (size_t)Ns[a] * HELM_MAXOP);
         }
+    for (int adj = 0; adj < 2; ++adj) {
+      Lv.z64[adj] = dalloc<double2>(op->allocs, (size_t)3 * Lv.nz * HELM_MAXOP);
+      if (dtype == HELM_C64) Lv.z32[adj] = dalloc<float2>(op->allocs, (size_t)3 * Lv.nz * HELM_MAXOP);
+    }
   }
   op->m_int_d = dalloc<double>(op->allocs, n_int);
   // reduction scratch: BLAS kernels use (KMAX+1) x blocks per RHS at stride pstride; the

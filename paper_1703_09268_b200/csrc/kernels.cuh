@@ -20,6 +20,7 @@ template <typename R> struct Geo {
   const cx<R>* lo[3];      // 1D tables (H or H^H), axis 0=x,1=y,2=z, nop tables each
   const cx<R>* dg[3];
   const cx<R>* up[3];
+  const cx<R>* zpk;        // packed z coefficients [op][z][lo, dg, up] (ghosts masked, R7)
 };
 
 // The 1D tables and omega^2 of RHS r's operator.
@@ -210,6 +211,20 @@ __global__ void k_cast(long long n, const Tin* __restrict__ a, Tout* __restrict_
   long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p < n) b[p] = (Tout)a[p];
 }
+// zpk[(o nz + z) 3 + {0,1,2}] = (lo_z (0 at z = 0), dg_z, up_z (0 at z = nz-1)) of operator o
+template <typename T>
+__global__ void k_zpack(int nz, int nop, const T* __restrict__ lo, const T* __restrict__ dg, const T* __restrict__ up,
+                        T* __restrict__ zpk) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nz * nop) return;
+  const int z = e % nz;
+  T zero;
+  zero.x = 0; zero.y = 0;
+  zpk[3 * e] = z > 0 ? lo[e] : zero;
+  zpk[3 * e + 1] = dg[e];
+  zpk[3 * e + 2] = z < nz - 1 ? up[e] : zero;
+}
+
 __global__ void k_cast_c(long long n, const double2* __restrict__ a, float2* __restrict__ b) {
   long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p < n) b[p] = make_float2((float)a[p].x, (float)a[p].y);
@@ -220,6 +235,8 @@ __global__ void k_cast_c(long long n, const double2* __restrict__ a, float2* __r
 template <typename R>
 __global__ void __launch_bounds__(HELM_RED_THREADS)
 k_norm_start(long long N, const cx<R>* __restrict__ b, const int* __restrict__ active, KCtx ctx, RedBuf rb) {
+  pdl_wait();
+  pdl_trigger();
   const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   const cx<R>* br = b + (long long)r * N;
   double s = 0.0;
@@ -240,6 +257,8 @@ template <typename Tin, typename Tout>
 __global__ void k_copy_scale(long long N, const Tin* __restrict__ in, Tout* __restrict__ out,
                              const double* __restrict__ scale, int sstride, const int* __restrict__ kact,
                              int jstep, const int* __restrict__ active) {
+  pdl_wait();
+  pdl_trigger();
   const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   const bool dead = kact && jstep >= kact[r];
   const double s = scale ? scale[(long long)r * sstride] : 1.0;
@@ -255,6 +274,8 @@ __global__ void k_copy_scale(long long N, const Tin* __restrict__ in, Tout* __re
 template <typename R>
 __global__ void k_restrict(int fx, int fy, int fz, int cxn, int cyn, int czn, int has_y, R fac,
                            const cx<R>* __restrict__ in, cx<R>* __restrict__ out, const int* __restrict__ active) {
+  pdl_wait();
+  pdl_trigger();
   const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   const long long Nc = (long long)cxn * cyn * czn, Nf = (long long)fx * fy * fz;
   const cx<R>* fin = in + (long long)r * Nf;
@@ -287,6 +308,8 @@ __global__ void k_restrict(int fx, int fy, int fz, int cxn, int cyn, int czn, in
 template <typename R>
 __global__ void k_prolong_add(int fx, int fy, int fz, int cxn, int cyn, int czn, int has_y,
                               const cx<R>* __restrict__ in, cx<R>* __restrict__ out, const int* __restrict__ active) {
+  pdl_wait();
+  pdl_trigger();
   const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   const long long Nc = (long long)cxn * cyn * czn, Nf = (long long)fx * fy * fz;
   const cx<R>* cin = in + (long long)r * Nc;
@@ -406,6 +429,8 @@ template <typename R, int NV>
 __global__ void __launch_bounds__(HELM_RED_THREADS)
 k_update_t(long long N, VPtrs<R> V, int j, cx<R>* __restrict__ w, const int* __restrict__ active, KCtx ctx,
            RedBuf rb) {
+  pdl_wait();
+  pdl_trigger();
   const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   if (j >= ctx.kact[r]) return;
   const long long off = (long long)r * N;
@@ -454,6 +479,8 @@ template <typename R, int K>
 __global__ void __launch_bounds__(HELM_RED_THREADS)
 k_solupdate_t(long long N, VPtrs<R> Z, const double* __restrict__ zscale, cx<R>* __restrict__ x, int init,
               const int* __restrict__ active, KCtx ctx) {
+  pdl_wait();
+  pdl_trigger();
   const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   __shared__ cx<R> yc[K];
   __shared__ int s_k;

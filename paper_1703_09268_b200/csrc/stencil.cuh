@@ -183,6 +183,8 @@ __device__ inline void plane_epilogue(const KCtx& ctx, int r, int jstep, const d
 template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC>
 __global__ void __launch_bounds__(BX * BY / PY)
 k_plane(const PlaneArgs<R> a) {
+  pdl_wait();
+  pdl_trigger();
   using C = cx<R>;
   using Sh = PlaneShape<MODE, NV>;
   constexpr int NX = Sh::NX, NP = Sh::NP, NVR = Sh::NVR;

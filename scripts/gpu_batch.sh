@@ -1,8 +1,13 @@
 set -x
-TAG=${TAG:-r1o}
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -3 gpurun_out/${TAG}_pytest_gpu.log
-HELM_DEBUG=1 timeout 300 python scripts/tune_plane.py cfg2 c128 >> gpurun_out/${TAG}_tune.jsonl 2>>gpurun_out/${TAG}_tune.err
-timeout 900 python bench.py --steps 2 --warmup 3 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"
-timeout 900 python bench.py --steps 2 --warmup 3 --dtype c64 --no-cpu-baseline --no-matvec > gpurun_out/${TAG}_bench_c64.json 2> gpurun_out/${TAG}_bench_c64.err; echo "bench c64 rc=$?"
+TAG=${TAG:-r1t}
+for v in cur b428 cur b428; do
+  if [ $v = cur ]; then unset HELM_LIB_VARIANT; else export HELM_LIB_VARIANT=$v; fi
+  timeout 300 python scripts/tune_plane.py cfg2 c128 150 >> gpurun_out/${TAG}_tune.jsonl 2>> gpurun_out/${TAG}_tune.err
+  timeout 300 python scripts/tune_plane.py cfg2 c128 50 >> gpurun_out/${TAG}_tune.jsonl 2>> gpurun_out/${TAG}_tune.err
+done
+unset HELM_LIB_VARIANT
+for i in 1 2; do
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-matvec > gpurun_out/${TAG}_bench$i.json 2> gpurun_out/${TAG}_bench$i.err
+python -c "import json;d=json.load(open('gpurun_out/${TAG}_bench$i.json'));print('bench', d['value'], d['level_shares'], d['roofline'])"
+done
 echo done

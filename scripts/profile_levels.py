@@ -19,20 +19,22 @@ from paper_1703_09268_b200 import api  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dtype", default="c128")
-    ap.add_argument("--freq", type=float, default=5.0)
+    ap.add_argument("--freq", type=float, default=0.0, help="one frequency (0 = the cfg2 set 3,5,7 Hz)")
     ap.add_argument("--nsrc", type=int, default=50)
+    ap.add_argument("--max-rhs", type=int, default=0)
     ap.add_argument("--stride", type=int, default=1)
     a = ap.parse_args()
-    p = synth.cfg2(nsrc=a.nsrc, freqs=(a.freq,))
+    p = synth.cfg2(nsrc=a.nsrc, freqs=(a.freq,) if a.freq > 0 else (3.0, 5.0, 7.0))
+    mr = a.max_rhs if a.max_rhs > 0 else a.nsrc * len(p.freqs)
     grid = api.Grid.of(p)
     pml = api.Pml(v_ref=3000.0)
     dt = api.C64 if a.dtype == "c64" else api.C128
-    d, _ = api.fwi_forward(grid, p.m_true, p.freqs, p.src, p.rec, pml, api.C128, api.SolveOpts(rtol=1e-8), max_rhs=a.nsrc)
-    api.fwi_misfit_grad(grid, p.m, p.freqs, p.src, p.rec, d, pml, dt, max_rhs=a.nsrc)   # warm
+    d, _ = api.fwi_forward(grid, p.m_true, p.freqs, p.src, p.rec, pml, api.C128, api.SolveOpts(rtol=1e-8), max_rhs=mr)
+    api.fwi_misfit_grad(grid, p.m, p.freqs, p.src, p.rec, d, pml, dt, max_rhs=mr)   # warm
     torch.cuda.synchronize()
     api.profile(True, a.stride)
     t0 = time.perf_counter()
-    fg, rep = api.fwi_misfit_grad(grid, p.m, p.freqs, p.src, p.rec, d, pml, dt, max_rhs=a.nsrc)
+    fg, rep = api.fwi_misfit_grad(grid, p.m, p.freqs, p.src, p.rec, d, pml, dt, max_rhs=mr)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     out = {"wall_s": wall, "cycles": sorted({r["outer_cycles"] for r in rep}), "levels": {}}

@@ -17,8 +17,9 @@ from paper_1703_09268_b200 import api  # noqa: E402
 
 what = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 dt = api.C64 if (len(sys.argv) > 2 and sys.argv[2] == "c64") else api.C128
+nrhs_arg = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 if what == "cfg2":
-    p, f, vref, nrhs = synth.cfg2(freqs=(5.0,)), 5.0, 3000.0, 50
+    p, f, vref, nrhs = synth.cfg2(freqs=(5.0,)), 5.0, 3000.0, nrhs_arg or 50
 elif what == "cfg3":
     p, f, vref, nrhs = synth.cfg3_batch(8), 8.0, 2000.0, 8
 else:
@@ -26,7 +27,7 @@ else:
 op = api.helm_setup(api.Grid.of(p), p.m, 2 * np.pi * f, api.Pml(v_ref=vref), dt, max_rhs=nrhs)
 levels = op.levels()
 Sc, Sr = (16, 8) if dt == api.C128 else (8, 4)
-out = {"case": what, "dtype": "c128" if dt == api.C128 else "c64", "env": {k: v for k, v in os.environ.items() if k.startswith("HELM_")},
+out = {"case": what, "nrhs": nrhs, "variant": os.environ.get("HELM_LIB_VARIANT", "cur"), "dtype": "c128" if dt == api.C128 else "c64", "env": {k: v for k, v in os.environ.items() if k.startswith("HELM_")},
        "rows": []}
 kinds = [(0, 0, 2), (1, 0, 3), (3, 0, 2), (3, 1, 4), (3, 2, 5), (3, 3, 6), (4, 4, 6), (2, 2, 5), (10, 5, 7), (11, 2, 5), (11, 4, 7), (12, 0, 1)]
 for l, (nx, ny, nz) in enumerate(levels):
