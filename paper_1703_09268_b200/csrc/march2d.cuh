@@ -53,77 +53,37 @@ template <typename R, int MODE, int NV> struct MarchShape {
   static constexpr int stage_bytes = (32 * (NX * (int)sizeof(cx<R>) + (int)sizeof(R)) + 15) / 16 * 16;
 };
 
-template <typename R, int MODE, int NV>
-__global__ void __launch_bounds__(128)
-k_march2d(const MarchArgs<R> a) {
-  pdl_wait();
-  pdl_trigger();
+// One march pass over the (strip, z-chunk) items of RHS r owned by warp `wi` of `nw`: the
+// streaming body shared by the grid-wide kernel (k_march2d) and the per-RHS persistent
+// GMRES kernel (k_gmres2d). Accumulates this warp's partial projections / norms.
+template <typename R, int MODE, int NV, int NVR>
+__device__ __forceinline__ void march_pass(const Geo<R>& g, const OpTab<R>& T, const cx<R>* ztr, long long rb0,
+                                           const cx<R>* xin, const cx<R>* bin, cx<R>* yout, cx<R>* vout,
+                                           const cx<R>* const* Vp, R sc, R cw, const cx<R> (&cv)[(MODE >= 3 && NV > 0) ? NV : 1],
+                                           int nstrip, int nzc, int zlen, int wi, int nw, int S, unsigned char* ring,
+                                           unsigned ring_s, double2 (&acc)[NVR], double& nrm, double& ynrm) {
   using C = cx<R>;
   using SH = MarchShape<R, MODE, NV>;
   constexpr int NB = SH::NB, NX = SH::NX, SB = SH::stage_bytes;
   constexpr bool FORM = MODE >= 3 && NV > 0;
   constexpr bool LAST = MODE == 4;
-  constexpr int NVR = MODE == 1 ? 1 : (MODE == 2 ? NV : (MODE >= 3 ? NV + 3 : 1));
-  const Geo<R>& g = a.g;
-  const int nx = g.nx, nz = g.nz, S = a.S;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
-  const int ia = gw / a.wpr, wi = gw % a.wpr;   // ia: index in the compact active-RHS list
-  const int r = ia < a.nrhs ? (a.active ? a.active[ia] : ia) : 0;
-  const long long N = g.N;
-  const long long rb0 = (long long)r * N;
+  const int nx = g.nx, nz = g.nz;
+  const int lane = threadIdx.x & 31;
   const C zero = mkc((R)0, (R)0);
-  // z coefficients of every operator of the level (packed, ghosts masked, R7) in shared
-  // memory: one contiguous copy per CTA
-  extern __shared__ __align__(16) unsigned char msm[];
-  C* zt = reinterpret_cast<C*>(msm);
-  for (int e = threadIdx.x; e < 3 * g.nop * nz; e += blockDim.x) zt[e] = g.zpk[e];
-  __syncthreads();
-  if (ia >= a.nrhs) return;
-  if (a.kact && a.jskip >= a.kact[r]) return;
-  const size_t zbytes = ((size_t)3 * g.nop * nz * sizeof(C) + 15) / 16 * 16;
-  unsigned char* ring = msm + zbytes + (size_t)wib * S * SB;
-  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
-
-  R sc = (R)1;
-  if ((MODE == 0 || MODE == 2) && a.xscale) sc = (R)a.xscale[(long long)r * a.sstride];
-  const OpTab<R> T = op_tab(g, r);
-  const C* ztr = zt + 3 * (long long)(g.rop ? g.rop[r] : 0) * nz;   // this RHS's z table
-  R cw = (R)1;
-  C cv[FORM ? NV : 1];
-  if constexpr (FORM) {
-    const double* s = a.ctx.scale + (long long)r * (HELM_KMAX + 1);
-    const double2* H = a.ctx.H + (long long)r * (HELM_KMAX + 1) * HELM_KMAX;
-    cw = (R)s[NV - 1];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const double2 h = H[hidx(i, NV - 1)];
-      cv[i] = mkc((R)(-h.x * s[i]), (R)(-h.y * s[i]));
-    }
-  }
-
-  double2 acc[NVR];
-#pragma unroll
-  for (int k = 0; k < NVR; ++k) acc[k] = make_double2(0.0, 0.0);
-  double nrm = 0.0, ynrm = 0.0;
-
-  // items (strip, z-chunk) of this RHS, strip fastest, dealt round-robin to its warps: warps
-  // on neighbouring strips stream the same depth together, so the cache lines shared at
-  // strip boundaries are read from HBM once (a balanced contiguous split lost up to 15 %)
-  const int nitems = a.nstrip * a.nzc;
-  for (int it = wi; it < nitems; it += a.wpr) {
-    const int strip = it % a.nstrip, zc = it / a.nstrip;
-    const int z0 = zc * a.zlen, z1 = min(nz, z0 + a.zlen);
+  const int nitems = nstrip * nzc;
+  for (int it = wi; it < nitems; it += nw) {
+    const int strip = it % nstrip, zc = it / nstrip;
+    const int z0 = zc * zlen, z1 = min(nz, z0 + zlen);
     const int x = strip * 30 - 1 + lane;
     const bool inx = x >= 0 && x < nx;
     const bool outp = lane >= 1 && lane <= 30 && inx;
     const long long xo = rb0 + (inx ? x : 0);
     const C lox = outp ? T.lo[0][x] : zero, upx = outp ? T.up[0][x] : zero, dgx = outp ? T.dg[0][x] : zero;
     const C* src[NX];
-    src[0] = a.x + xo;
+    src[0] = xin + xo;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) src[1 + i] = a.V.p[i] + xo;
-    if constexpr (MODE == 1) src[NX - 1] = a.b + xo;
+    for (int i = 0; i < NB; ++i) src[1 + i] = Vp[i] + xo;
+    if constexpr (MODE == 1) src[NX - 1] = bin + xo;
     const R* msrc = g.m + (inx ? x : 0);
 
     // plane q (may be a ghost plane: zero-filled, R7) into ring slot `sl`; one commit group
@@ -175,26 +135,26 @@ k_march2d(const MarchArgs<R> a) {
       if (outp) {
         const long long o = xo + (long long)z * nx;
         if constexpr (MODE == 0) {
-          a.y[o] = cscale(hx, sc);
+          yout[o] = cscale(hx, sc);
         } else if constexpr (MODE == 1) {
           const C rv = csub(opnd(s0, NX - 1), hx);
-          a.y[o] = rv;
+          yout[o] = rv;
           nrm += (double)rv.x * rv.x + (double)rv.y * rv.y;
         } else if constexpr (MODE == 2) {
           const C w = cscale(hx, sc);
-          a.y[o] = w;
+          yout[o] = w;
           const double2 wd = to_d(w);
 #pragma unroll
           for (int i = 0; i < NV; ++i) acc[i] = cdot_acc(acc[i], to_d(opnd(s0, 1 + i)), wd);
         } else {
           const double2 hd = to_d(hx);
           if constexpr (LAST) ynrm += hd.x * hd.x + hd.y * hd.y;
-          else a.y[o] = hx;
+          else yout[o] = hx;
 #pragma unroll
           for (int i = 0; i < NV; ++i) acc[i] = cdot_acc(acc[i], to_d(opnd(s0, 1 + i)), hd);
           acc[NV] = cdot_acc(acc[NV], to_d(f0), hd);
           if constexpr (NV > 0) {
-            a.vout[o] = f0;
+            vout[o] = f0;
             nrm += (double)f0.x * f0.x + (double)f0.y * f0.y;
           }
         }
@@ -208,6 +168,68 @@ k_march2d(const MarchArgs<R> a) {
     cpa_wait<0>();
     __syncwarp();
   }
+}
+
+// Forming coefficients of fused step NV (MODE 3/4): V_NV = cw W + sum_i cv_i V_i.
+template <typename R, int NV>
+__device__ __forceinline__ void form_coeffs(const KCtx& ctx, int r, R& cw, cx<R> (&cv)[NV > 0 ? NV : 1]) {
+  if constexpr (NV > 0) {
+    const double* s = ctx.scale + (long long)r * (HELM_KMAX + 1);
+    const double2* H = ctx.H + (long long)r * (HELM_KMAX + 1) * HELM_KMAX;
+    cw = (R)s[NV - 1];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double2 h = H[hidx(i, NV - 1)];
+      cv[i] = mkc((R)(-h.x * s[i]), (R)(-h.y * s[i]));
+    }
+  }
+}
+
+template <typename R, int MODE, int NV>
+__global__ void __launch_bounds__(128)
+k_march2d(const MarchArgs<R> a) {
+  pdl_wait();
+  pdl_trigger();
+  using C = cx<R>;
+  using SH = MarchShape<R, MODE, NV>;
+  constexpr int SB = SH::stage_bytes;
+  constexpr bool FORM = MODE >= 3 && NV > 0;
+  constexpr int NVR = MODE == 1 ? 1 : (MODE == 2 ? NV : (MODE >= 3 ? NV + 3 : 1));
+  const Geo<R>& g = a.g;
+  const int nz = g.nz, S = a.S;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
+  const int ia = gw / a.wpr, wi = gw % a.wpr;   // ia: index in the compact active-RHS list
+  const int r = ia < a.nrhs ? (a.active ? a.active[ia] : ia) : 0;
+  // z coefficients of every operator of the level (packed, ghosts masked, R7) in shared
+  // memory: one contiguous copy per CTA
+  extern __shared__ __align__(16) unsigned char msm[];
+  C* zt = reinterpret_cast<C*>(msm);
+  for (int e = threadIdx.x; e < 3 * g.nop * nz; e += blockDim.x) zt[e] = g.zpk[e];
+  __syncthreads();
+  if (ia >= a.nrhs) return;
+  if (a.kact && a.jskip >= a.kact[r]) return;
+  const size_t zbytes = ((size_t)3 * g.nop * nz * sizeof(C) + 15) / 16 * 16;
+  unsigned char* ring = msm + zbytes + (size_t)wib * S * SB;
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+
+  R sc = (R)1;
+  if ((MODE == 0 || MODE == 2) && a.xscale) sc = (R)a.xscale[(long long)r * a.sstride];
+  const OpTab<R> T = op_tab(g, r);
+  const C* ztr = zt + 3 * (long long)(g.rop ? g.rop[r] : 0) * nz;   // this RHS's z table
+  R cw = (R)1;
+  C cv[FORM ? NV : 1];
+  if constexpr (FORM) form_coeffs<R, NV>(a.ctx, r, cw, cv);
+
+  double2 acc[NVR];
+#pragma unroll
+  for (int k = 0; k < NVR; ++k) acc[k] = make_double2(0.0, 0.0);
+  double nrm = 0.0, ynrm = 0.0;
+  // items (strip, z-chunk) of this RHS, strip fastest, dealt round-robin to its warps: warps
+  // on neighbouring strips stream the same depth together, so the cache lines shared at
+  // strip boundaries are read from HBM once (a balanced contiguous split lost up to 15 %)
+  march_pass<R, MODE, NV, NVR>(g, T, ztr, (long long)r * g.N, a.x, a.b, a.y, a.vout, a.V.p, sc, cw, cv, a.nstrip,
+                               a.nzc, a.zlen, wi, a.wpr, S, ring, ring_s, acc, nrm, ynrm);
 
   if constexpr (MODE != 0) {
     if constexpr (MODE == 1) acc[0] = make_double2(nrm, 0.0);

@@ -1,13 +1,11 @@
 set -x
-TAG=${TAG:-r1t}
-for v in cur b428 cur b428; do
-  if [ $v = cur ]; then unset HELM_LIB_VARIANT; else export HELM_LIB_VARIANT=$v; fi
-  timeout 300 python scripts/tune_plane.py cfg2 c128 150 >> gpurun_out/${TAG}_tune.jsonl 2>> gpurun_out/${TAG}_tune.err
-  timeout 300 python scripts/tune_plane.py cfg2 c128 50 >> gpurun_out/${TAG}_tune.jsonl 2>> gpurun_out/${TAG}_tune.err
+TAG=${TAG:-r1w}
+for g in 1 0 1 0; do
+HELM_GMRES_CTA=$g timeout 600 python scripts/vcycle_gap.py 150 5 2>/dev/null | head -1 | sed "s/^/cta=$g /"
+HELM_GMRES_CTA=$g timeout 600 python scripts/vcycle_gap.py 50 5 2>/dev/null | head -1 | sed "s/^/cta=$g /"
 done
-unset HELM_LIB_VARIANT
-for i in 1 2; do
-timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-matvec > gpurun_out/${TAG}_bench$i.json 2> gpurun_out/${TAG}_bench$i.err
-python -c "import json;d=json.load(open('gpurun_out/${TAG}_bench$i.json'));print('bench', d['value'], d['level_shares'], d['roofline'])"
+for g in 1 0; do
+HELM_GMRES_CTA=$g timeout 900 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-matvec > gpurun_out/${TAG}_bench_cta$g.json 2> gpurun_out/${TAG}_bench_cta$g.err
+python -c "import json;d=json.load(open('gpurun_out/${TAG}_bench_cta$g.json'));print('bench cta=$g', d['value'], d['level_shares'], d['kernel_shares'])"
 done
 echo done

@@ -45,6 +45,8 @@ elif what == "probe":
     case, level, kind, nv = sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
     if case == "cfg2":
         p, f, vref, nrhs = synth.cfg2(freqs=(5.0,)), 5.0, 3000.0, 50
+    elif case == "cfg2_150":
+        p, f, vref, nrhs = synth.cfg2(freqs=(5.0,)), 5.0, 3000.0, 150
     else:
         p, f, vref, nrhs = synth.cfg5(256), 6.0, 4500.0, 1
     op = api.helm_setup(api.Grid.of(p), p.m, 2 * np.pi * f, api.Pml(v_ref=vref), api.C128, max_rhs=nrhs)
