@@ -2,7 +2,7 @@
 // level hierarchy, Krylov workspace), the FGMRES / ML-GMRES orchestration and the C ABI
 // declared in include/helm.h. All numerics run in the kernels of kernels.cuh.
 #include "helm.h"
-#include "gmres2d.cuh"
+#include "march2d.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -41,7 +41,7 @@ constexpr int K1 = HELM_KMAX + 1;
 
 // ------------------------------------------------------------------------------ probes
 enum KClass { KC_STENCIL = 0, KC_RESID, KC_NORM, KC_DOTS, KC_UPDATE, KC_SOLUPD, KC_COPY, KC_RESTRICT,
-              KC_PROLONG, KC_FWI, KC_SETUP, KC_GMRES };
+              KC_PROLONG, KC_FWI, KC_SETUP };
 struct ProbeRec { int cls, level; cudaEvent_t a, b; double bytes; };
 struct Prof {
   bool on = false;
@@ -409,78 +409,6 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
   pdl_launch(kern, dim3((unsigned)((warps + 3) / 4)), dim3(128), smem, st, a);
 }
 
-// 2D coarse levels: the whole restarted GMRES(ko, ki) of a smoother / the coarsest solve in
-// one launch, one CTA per active RHS (gmres2d.cuh). HELM_GMRES_CTA=0 falls back to the
-// grid-wide kernel sequence.
-// HELM_GMRES_CTA: 0 off (default), 1 coarsest level only, 2 every coarse level. Measured on
-// B200 (cfg2, 50 / 150 RHS): level-0 V-cycle 29.1 / 66.8 ms off, 30.3 / 66.8 ms with 1, and
-// 77.7 ms (150 RHS) with 2 — one CTA per RHS is latency-bound (each warp is a serial chain
-// of plane steps) and cannot pull the bandwidth of the grid-wide kernels.
-bool gmres_cta_ok(const helm_op* op, int l, int ki) {
-  static const int mode = env_int("HELM_GMRES_CTA", 0);
-  if (!mode || l < 1 || op->lev[l].ny != 1 || ki > HELM_GMRES_CTA_KI) return false;
-  return mode == 2 || l == op->L - 1;
-}
-
-template <typename R>
-void run_gmres2d(helm_op* op, int l, int adj, int nrhs, KCtx& ctx, int ko, int ki, const cx<R>* b, cx<R>* x,
-                 bool x0zero, cx<R>* const* V, cx<R>* Wx) {
-  if (!op->nact) return;
-  auto kern = k_gmres2d<R>;
-  constexpr int SBMAX = MarchShape<R, 3, HELM_GMRES_CTA_KI - 1>::stage_bytes;
-  GmresArgs<R> a{};
-  a.g = geo<R>(op, l, adj);
-  a.b = b; a.x = x; a.Wx = Wx;
-  for (int i = 0; i <= ki; ++i) a.V[i] = V[i];
-  a.active = op->active_d; a.nrhs = op->nact;
-  a.ko = ko; a.ki = ki; a.x0zero = x0zero ? 1 : 0;
-  a.nstrip = (a.g.nx + 29) / 30;
-  ctx.k = ki;
-  a.ctx = ctx;
-  const size_t zbytes = ((size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>) + 15) / 16 * 16;
-  const size_t rbytes = (size_t)HELM_GMRES_WARPS * (HELM_KMAX + 3) * sizeof(double2);
-  // two CTAs per SM: ~110 KB each
-  int S = (int)(((110 * 1024) - (long long)zbytes - (long long)rbytes) / (HELM_GMRES_WARPS * SBMAX));
-  S = std::max(3, std::min(S, 12));
-  a.S = S;
-  const size_t smem = zbytes + rbytes + (size_t)HELM_GMRES_WARPS * S * SBMAX;
-  static size_t attr_max = 48 * 1024;
-  if (smem > attr_max) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_max = smem;
-  }
-  const int nz = a.g.nz, wpr = HELM_GMRES_WARPS;
-  long long best = -1;
-  int nzc_b = 1, zl_b = nz;
-  for (int n = 1; n <= nz; ++n) {
-    const int zl = (nz + n - 1) / n, nzc = (nz + zl - 1) / zl;
-    if (nzc != n) continue;
-    const long long items = (long long)a.nstrip * nzc;
-    const long long cost = ((items + wpr - 1) / wpr) * (zl + 2 + S / 2);
-    if (best < 0 || cost < best) { best = cost; nzc_b = nzc; zl_b = zl; }
-  }
-  a.nzc = nzc_b; a.zlen = zl_b;
-  prof_begin(KC_GMRES, op->st, l);
-  pdl_launch(kern, dim3((unsigned)op->nact), dim3(HELM_GMRES_WARPS * 32), smem, op->st, a);
-  CKL();
-  // accounting: the same algorithmic bytes / matvecs as the grid-wide sequence (per RHS;
-  // acct adds them to every active RHS)
-  const double N = (double)op->lev[l].N, Sc = sizeof(cx<R>), Sr = sizeof(R);
-  double bytes = 0.0;
-  for (int cyc = 0; cyc < ko; ++cyc) {
-    const bool fz = cyc == 0 && x0zero;
-    if (!fz) acct(op, l, 0.0, true, nrhs);   // the restart residual is a matvec
-    bytes += fz ? Sc * N : (3 * Sc + Sr) * N;
-    for (int j = 0; j < ki; ++j) {
-      const double per = j < ki - 1 ? (j == 0 ? 2 : j + 3) * Sc + Sr : (j == 0 ? 1 : j + 2) * Sc + Sr;
-      acct(op, l, 0.0, true, nrhs);
-      bytes += per * N;
-    }
-    bytes += (ki + (fz ? 1.0 : 2.0)) * Sc * N;
-  }
-  prof_end(KC_GMRES, op->st, acct(op, l, bytes, false, nrhs));
-}
-
 // Plane-streaming stencil (stencil.cuh). mode 0: y = s H x; 1: y = b - H x (+cycle start);
 // 2: y = s H x with the fused projections h_ij = <V_i, y>, i < nv (nv = j + 1);
 // 3: fused Arnoldi step nv of unpreconditioned GMRES (x = raw W or V_0, V = basis, vout);
@@ -651,10 +579,6 @@ void krylov(helm_op* op, int l, int adj, int nrhs, KCtx& ctx, int ko, int ki, bo
     } else {
       launch_stencil<R>(op, l, adj, 1, nrhs, x, V[0], b, nullptr, nullptr, 0, ctx);
       v0 = V[0];
-    }
-    if (!flex && cyc == 0 && gmres_cta_ok(op, l, ki)) {   // whole GMRES(ko, ki) in one launch
-      run_gmres2d<R>(op, l, adj, nrhs, ctx, ko, ki, b, x, x0zero, V, Wx);
-      return;
     }
     if (!flex) {
       cx<R>* Wb[2] = {V[ki], Wx};

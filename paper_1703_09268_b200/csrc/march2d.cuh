@@ -54,8 +54,7 @@ template <typename R, int MODE, int NV> struct MarchShape {
 };
 
 // One march pass over the (strip, z-chunk) items of RHS r owned by warp `wi` of `nw`: the
-// streaming body shared by the grid-wide kernel (k_march2d) and the per-RHS persistent
-// GMRES kernel (k_gmres2d). Accumulates this warp's partial projections / norms.
+// streaming body of k_march2d. Accumulates this warp's partial projections / norms.
 template <typename R, int MODE, int NV, int NVR>
 __device__ __forceinline__ void march_pass(const Geo<R>& g, const OpTab<R>& T, const cx<R>* ztr, long long rb0,
                                            const cx<R>* xin, const cx<R>* bin, cx<R>* yout, cx<R>* vout,
