@@ -3,6 +3,7 @@
 // declared in include/helm.h. All numerics run in the kernels of kernels.cuh.
 #include "helm.h"
 #include "march2d.cuh"
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -306,6 +307,39 @@ const PlaneTune& plane_tune() {
   return t;
 }
 
+// TMA tensor map of a batched complex vector [rhs][z][y][x] viewed as reals (x fastest:
+// 2 nx reals per row), box = the 34 x 10 halo'd tile (x0-1 .. x0+32, y0-1 .. y0+8) of one
+// plane of one RHS. Needs 16-B aligned base and row pitch (always for complex128; nx even
+// for complex64). Returns false when TMA cannot describe the array.
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+template <typename R>
+bool make_tile_map(CUtensorMap* m, const void* base, int nx, int ny, int nz, int nrhs) {
+  auto enc = tma_encoder();
+  if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  const cuuint64_t eb = sizeof(R);
+  if ((2 * (cuuint64_t)nx * eb) % 16) return false;
+  cuuint64_t dims[4] = {2 * (cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz, (cuuint64_t)nrhs};
+  cuuint64_t strides[3] = {2 * (cuuint64_t)nx * eb, 2 * (cuuint64_t)nx * ny * eb, 2 * (cuuint64_t)nx * ny * nz * eb};
+  cuuint32_t box[4] = {68, 10, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  const CUresult rc = enc(m, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                          const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return rc == CUDA_SUCCESS;
+}
+
 struct PlaneCfg { int S = 0, occ = 0; size_t smem = 0; };
 
 // Split of a group's T tiles x nz planes over its CTAs (one resident wave of G CTAs over
@@ -339,7 +373,7 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
     const PlaneTune& t = plane_tune();
     c.S = t.s_fixed >= 4 ? std::min(t.s_fixed, 12) : (int)std::min<size_t>(12, (220 * 1024) / (t.occ_target * sb));
     c.S = std::max(c.S, 4);
-    c.smem = c.S * sb;
+    c.smem = c.S * sb + 8 * c.S;   // ring + one mbarrier per stage (TMA)
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ, kern, NT, c.smem));
     if (c.occ < 1) throw HelmErr{HELM_ERR_STATE, "plane kernel does not fit on an SM"};
@@ -455,6 +489,16 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
   a.ntx = (a.g.nx + 31) / 32;
   a.nty = (a.g.ny + 7) / 8;
   const int groups = op->nact;
+  // TMA for the halo'd tiles when every halo'd operand can be described (HELM_TMA=0: cp.async)
+  static const bool tma_on = env_int("HELM_TMA", 1) != 0;
+  a.tma = 0;
+  if (tma_on) {
+    const int nxt = mode >= 3 ? nv + 1 : 1;
+    bool ok = true;
+    for (int t = 0; t < nxt && ok; ++t)
+      ok = make_tile_map<R>(&a.tm[t], t == 0 ? (const void*)x : (const void*)a.V.p[t - 1], a.g.nx, a.g.ny, a.g.nz, nrhs);
+    a.tma = ok ? 1 : 0;
+  }
   const long long units = (long long)a.ntx * a.nty * a.g.nz;
   prof_begin(cls, op->st, l);
   if (mode == 0) run_plane<R, 0, 0, true>(a, groups, units, op->st);

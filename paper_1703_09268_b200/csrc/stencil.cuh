@@ -27,7 +27,35 @@
 //         The last CTA per RHS finalises column NV-1 (h_{NV,NV-1} = ||V_NV||, Givens,
 //         breakdown guard) and stores column NV: h_{i,NV} = s_i s_NV <V_i, Y>.
 #pragma once
+#include <cuda.h>   // CUtensorMap (the map is encoded on the host through the driver entry point)
 #include "kernels.cuh"
+
+// ---- TMA + mbarrier (3D halo'd tiles): one elected thread issues cp.async.bulk.tensor per
+// operand and stage; out-of-bounds box elements are zero-filled = the Dirichlet ghosts (R7).
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load4(unsigned dst, const CUtensorMap* map, unsigned bar, int c0, int c1, int c2,
+                                          int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
 template <int B> __device__ __forceinline__ void cpa(unsigned s, const void* gmem, bool pred) {
   const int sz = pred ? B : 0;
@@ -71,6 +99,8 @@ template <typename R> struct PlaneArgs {
   int cpg;                 // CTAs per group
   int nzc, zlen;           // z-chunks per tile and their length
   int S;                   // ring stages (>= 4)
+  int tma;                 // halo'd tiles by TMA (tm[0] = x / W, tm[1 + i] = V_i) instead of cp.async
+  CUtensorMap tm[HELM_KMAX + 1];
   KCtx ctx;
   RedBuf rb;
 };
@@ -182,7 +212,7 @@ __device__ inline void plane_epilogue(const KCtx& ctx, int r, int jstep, const d
 
 template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC>
 __global__ void __launch_bounds__(BX * BY / PY)
-k_plane(const PlaneArgs<R> a) {
+k_plane(const __grid_constant__ PlaneArgs<R> a) {
   pdl_wait();
   pdl_trigger();
   using C = cx<R>;
@@ -238,6 +268,17 @@ k_plane(const PlaneArgs<R> a) {
   }
 
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
+  // TMA: one mbarrier per ring stage, after the stages (stage addresses stay 128-B aligned)
+  const unsigned mbase = sbase + (unsigned)(S * SM::stage_bytes);
+  const bool tma = a.tma != 0;
+  if (tma) {
+    if (threadIdx.x == 0) {
+      for (int s2 = 0; s2 < S; ++s2) mbar_init(mbase + 8 * s2, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
+  unsigned pbits = 0;      // parity of the next TMA fill of each stage
   double2 acc[NVR];
 #pragma unroll
   for (int k = 0; k < NVR; ++k) acc[k] = make_double2(0.0, 0.0);
@@ -302,15 +343,29 @@ k_plane(const PlaneArgs<R> a) {
         const bool zin = z >= 0 && z < nz;
         const unsigned st = sbase + (unsigned)(stg * SM::stage_bytes);
         const long long zo = (long long)z * plane;
+        if (tma) {
+          if (threadIdx.x == 0) {
+            fence_proxy_async();   // the stage's previous contents were read / formed by the generic proxy
+            const unsigned bar = mbase + 8 * stg;
+            mbar_expect_tx(bar, (unsigned)(NX * SM::XE * sizeof(C)));
+            constexpr int CR = (int)(sizeof(C) / sizeof(R));   // tensor element = one real
 #pragma unroll
-        for (int t = 0; t < NX; ++t) {
-          const C* src = t == 0 ? a.x : a.V.p[t - 1];
+            for (int t = 0; t < NX; ++t)
+              tma_load4(st + (unsigned)(t * SM::XE * sizeof(C)), &a.tm[t], bar, CR * (txb * BX - 1), tyb * BY - YH, z,
+                        rhs[0]);
+          }
+          pbits ^= 1u << stg;
+        } else {
 #pragma unroll
-          for (int i = 0; i < NL; ++i)
-            if (lh[i]) {
-              const bool p = lp[i] && zin;
-              cpa<sizeof(C)>(st + (unsigned)(t * SM::XE * sizeof(C)) + ls[i], p ? src + lg[i] + zo : a.x, p);
-            }
+          for (int t = 0; t < NX; ++t) {
+            const C* src = t == 0 ? a.x : a.V.p[t - 1];
+#pragma unroll
+            for (int i = 0; i < NL; ++i)
+              if (lh[i]) {
+                const bool p = lp[i] && zin;
+                cpa<sizeof(C)>(st + (unsigned)(t * SM::XE * sizeof(C)) + ls[i], p ? src + lg[i] + zo : a.x, p);
+              }
+          }
         }
         if (q >= 1 && z < z1) {
           if ((YC ? threadIdx.x : tx) < 3) {   // z coefficients of plane z: lo, dg, up (ghosts masked, R7)
@@ -381,6 +436,14 @@ k_plane(const PlaneArgs<R> a) {
     for (int z = z0; z < z1; ++z) {
       const int q = z - z0 + 1;
       cpa_wait_n(S - 4);        // this thread's groups <= q+1 complete (committed: <= q+S-3)
+      if (tma) {                // ... and the TMA tiles of planes <= q+1 (stage s_m1 + 2)
+        const int sw = inc(inc(s_m1));
+        if (z == z0) {
+          mbar_wait(mbase + 8 * s_m1, ((pbits >> s_m1) & 1u) ^ 1u);
+          mbar_wait(mbase + 8 * inc(s_m1), ((pbits >> inc(s_m1)) & 1u) ^ 1u);
+        }
+        mbar_wait(mbase + 8 * sw, ((pbits >> sw) & 1u) ^ 1u);
+      }
       csync<YC>();              // ... for every thread; stage (q-2)%S is free again
       load(q + S - 2, s_ld);    // S-3 planes in flight while plane z is computed
       s_ld = inc(s_ld);
