@@ -309,8 +309,8 @@ const PlaneTune& plane_tune() {
 
 // TMA tensor map of a batched complex vector [rhs][z][y][x] viewed as reals (x fastest:
 // 2 nx reals per row), box = the 34 x 10 halo'd tile (x0-1 .. x0+32, y0-1 .. y0+8) of one
-// plane of one RHS. Needs 16-B aligned base and row pitch (always for complex128; nx even
-// for complex64). Returns false when TMA cannot describe the array.
+// plane of one RHS. Needs 16-B aligned base and row pitch (always for complex128). Returns
+// false when TMA is not used for the array.
 PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
@@ -326,6 +326,9 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
 template <typename R>
 bool make_tile_map(CUtensorMap* m, const void* base, int nx, int ny, int nz, int nrhs) {
   auto enc = tma_encoder();
+  // complex128 only: the FLOAT32 (complex64) maps faulted with an illegal instruction on
+  // B200 in this build; complex64 keeps the per-thread cp.async halo path
+  if (sizeof(R) != 8) return false;
   if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
   const cuuint64_t eb = sizeof(R);
   if ((2 * (cuuint64_t)nx * eb) % 16) return false;

@@ -109,9 +109,11 @@ template <typename R, int BX, int BY, int NX, int NP, bool YC>
 struct PlaneSmem {
   static constexpr int YH = YC ? 1 : 0;              // y-halo rows (3D only)
   static constexpr int XE = (BY + 2 * YH) * (BX + 2); // halo tile elements
+  // tile stride in elements, padded to 128 B (TMA destinations must be 128-B aligned)
+  static constexpr int XS = (int)(((XE * sizeof(cx<R>) + 127) / 128 * 128) / sizeof(cx<R>));
   static constexpr int PE = BY * BX;                 // own-point elements
   static constexpr size_t x_off = 0;
-  static constexpr size_t m_off = (size_t)NX * XE * sizeof(cx<R>);
+  static constexpr size_t m_off = (size_t)NX * XS * sizeof(cx<R>);
   static constexpr size_t p_off = m_off + PE * sizeof(R);
   static constexpr size_t z_off = p_off + (size_t)NP * PE * sizeof(cx<R>);
   static constexpr int ZR = YC ? 1 : BY;               // z-coefficient triples (2D: one per warp)
@@ -347,11 +349,11 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           if (threadIdx.x == 0) {
             fence_proxy_async();   // the stage's previous contents were read / formed by the generic proxy
             const unsigned bar = mbase + 8 * stg;
-            mbar_expect_tx(bar, (unsigned)(NX * SM::XE * sizeof(C)));
+            mbar_expect_tx(bar, (unsigned)(NX * SM::XE * sizeof(C)));   // full boxes (OOB zero-filled)
             constexpr int CR = (int)(sizeof(C) / sizeof(R));   // tensor element = one real
 #pragma unroll
             for (int t = 0; t < NX; ++t)
-              tma_load4(st + (unsigned)(t * SM::XE * sizeof(C)), &a.tm[t], bar, CR * (txb * BX - 1), tyb * BY - YH, z,
+              tma_load4(st + (unsigned)(t * SM::XS * sizeof(C)), &a.tm[t], bar, CR * (txb * BX - 1), tyb * BY - YH, z,
                         rhs[0]);
           }
           pbits ^= 1u << stg;
@@ -363,7 +365,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
             for (int i = 0; i < NL; ++i)
               if (lh[i]) {
                 const bool p = lp[i] && zin;
-                cpa<sizeof(C)>(st + (unsigned)(t * SM::XE * sizeof(C)) + ls[i], p ? src + lg[i] + zo : a.x, p);
+                cpa<sizeof(C)>(st + (unsigned)(t * SM::XS * sizeof(C)) + ls[i], p ? src + lg[i] + zo : a.x, p);
               }
           }
         }
@@ -397,7 +399,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
         auto f1 = [&](int e) {
           C v = cscale(X[e], cw);
 #pragma unroll
-          for (int i = 0; i < NV; ++i) v = cfma(cv[i], X[(i + 1) * SM::XE + e], v);
+          for (int i = 0; i < NV; ++i) v = cfma(cv[i], X[(i + 1) * SM::XS + e], v);
           X[e] = v;
         };
         if constexpr (YC) {
@@ -493,7 +495,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           if constexpr (LAST) ynrm += hd.x * hd.x + hd.y * hd.y;
           else *yp = hx;
 #pragma unroll
-          for (int v = 0; v < NV; ++v) acc[v] = cdot_acc(acc[v], to_d(X1[(v + 1) * SM::XE + c]), hd);
+          for (int v = 0; v < NV; ++v) acc[v] = cdot_acc(acc[v], to_d(X1[(v + 1) * SM::XS + c]), hd);
           acc[NV] = cdot_acc(acc[NV], to_d(cur), hd);
           if constexpr (NV > 0) {
             a.vout[gofs[k] + zo] = cur;

@@ -1,9 +1,9 @@
 set -x
-TAG=${TAG:-r1z}
+TAG=${TAG:-r1z3}
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -3 gpurun_out/${TAG}_pytest_gpu.log
 for t in 1 0; do
-HELM_TMA=$t timeout 600 python scripts/matvec_sweep.py --N 256,512 --dtype c128,c64 --b 1,4 > gpurun_out/${TAG}_mv_tma$t.jsonl 2>&1
+HELM_TMA=$t timeout 600 python scripts/matvec_sweep.py --N 256,512 --dtype c128 --b 1,4 > gpurun_out/${TAG}_mv_tma$t.jsonl 2>&1
 python - <<PY
 import json
 for l in open('gpurun_out/${TAG}_mv_tma$t.jsonl'):
