@@ -188,7 +188,18 @@ struct helm_op {
   std::vector<int64_t> mv[4];
   double ws_vectors = 0.0;
   bool apply_only = false;
+  // captured level-0 V-cycles (CUDA graphs), keyed by (adjoint, batch size, active count)
+  struct VGraph { int adj, nrhs, nact; cudaGraphExec_t exec; double bytes; long long mv[4]; long long launches; };
+  std::vector<VGraph> vgraphs;
+  cudaStream_t cap_st = nullptr;   // private stream for graph capture (the caller's may be legacy)
+  bool graphs_off = false;         // a capture failed: run V-cycles live from then on
+  void clear_graphs() {
+    for (auto& g : vgraphs) cudaGraphExecDestroy(g.exec);
+    vgraphs.clear();
+  }
   ~helm_op() {
+    clear_graphs();
+    if (cap_st) cudaStreamDestroy(cap_st);
     for (void* p : allocs) cudaFree(p);
   }
 };
@@ -773,7 +784,7 @@ void alloc_ws(helm_op* op) {
       W[l].VB = dalloc<cx<R>>(op->allocs, n);
       W[l].ctxS = make_ctx(op->allocs, B, o.ks_i);
       vec += (o.ks_i + 3) * f;
-      if (l == 0 && op->dtype == HELM_C64) { W[l].VX = dalloc<cx<R>>(op->allocs, n); vec += f; }
+      if (l == 0) { W[l].VX = dalloc<cx<R>>(op->allocs, n); vec += f; }   // fixed V-cycle output (graphs)
     }
     if (l >= 1) {          // coarse solves
       for (int i = 0; i <= o.kc_i; ++i) W[l].FV[i] = dalloc<cx<R>>(op->allocs, n);
@@ -806,6 +817,7 @@ void validate_grid(const helm_grid* g) {
 }
 
 void op_set_model(helm_op* op, const double* m_host) {
+  op->clear_graphs();
   const helm_grid& G = op->grid;
   const size_t n_int = (size_t)G.n[0] * G.n[1] * G.n[2];
   CK(cudaMemcpyAsync(op->m_int_d, m_host, n_int * sizeof(double), cudaMemcpyHostToDevice, op->st));
@@ -815,6 +827,7 @@ void op_set_model(helm_op* op, const double* m_host) {
 void op_set_omegas(helm_op* op, const double* w, int n) {
   REQ(n >= 1 && n <= HELM_MAXOP, HELM_ERR_ARG, "too many operators in one batch");
   for (int o = 0; o < n; ++o) REQ(w[o] > 0 && std::isfinite(w[o]), HELM_ERR_ARG, "omega must be > 0");
+  op->clear_graphs();   // the captured kernels carry omega^2 and the operator count by value
   op->nop = n;
   for (int o = 0; o < n; ++o) op->omegas[o] = w[o];
   op->omega = w[0];
@@ -956,6 +969,80 @@ void set_active(helm_op* op, int nrhs) {
     CK(cudaMemcpyAsync(op->active_d, op->alist_h.data(), sizeof(int) * op->nact, cudaMemcpyHostToDevice, op->st));
 }
 
+// Level-0 V-cycle as a replayed CUDA graph: within a solve the launch sequence of a V-cycle
+// depends only on (adjoint, batch size, number of active RHS) — every Krylov scalar and the
+// active list live in device memory — so it is captured once per key and replayed (no
+// per-kernel host launch cost, tighter device-side launches). The graph writes a fixed
+// output buffer. Host-side accounting of the captured launches is recorded at capture and
+// added per replay. HELM_GRAPHS=0, or an active kernel profiler, runs the V-cycle live.
+template <typename R>
+void vcycle0_graph(helm_op* op, int adj, int nrhs, const cx<R>* b, cx<R>* z) {
+  static const bool on = env_int("HELM_GRAPHS", 1) != 0;
+  if (!on || g_prof.on || op->graphs_off || op->nact == 0) { vcycle<R>(op, 0, adj, nrhs, b, z); return; }
+  for (auto& g : op->vgraphs)
+    if (g.adj == adj && g.nrhs == nrhs && g.nact == op->nact) {
+      CK(cudaGraphLaunch(g.exec, op->st));
+      for (int r = 0; r < nrhs; ++r)
+        if (op->act_h[r]) {
+          op->bytes[r] += g.bytes;
+          for (int l = 0; l < 4; ++l) op->mv[l][r] += g.mv[l];
+        }
+      g_launches += g.launches;
+      return;
+    }
+  vcycle<R>(op, 0, adj, nrhs, b, z);   // this call runs live; the next ones replay
+  int r0 = 0;
+  while (r0 < nrhs && !op->act_h[r0]) ++r0;
+  const double b0 = op->bytes[r0];
+  long long m0[4];
+  for (int l = 0; l < 4; ++l) m0[l] = op->mv[l][r0];
+  std::vector<double> bsave = op->bytes;
+  std::vector<int64_t> msave[4];
+  for (int l = 0; l < 4; ++l) msave[l] = op->mv[l];
+  const long long l0 = g_launches;
+  cudaGraph_t graph = nullptr;
+  if (!op->cap_st) CK(cudaStreamCreateWithFlags(&op->cap_st, cudaStreamNonBlocking));
+  cudaStream_t user_st = op->st;
+  op->st = op->cap_st;   // capture on the private stream (nothing executes during capture)
+  bool ok = cudaStreamBeginCapture(op->st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    try {
+      vcycle<R>(op, 0, adj, nrhs, b, z);
+    } catch (...) {
+      ok = false;
+    }
+    cudaGraph_t g2 = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(op->st, &g2);
+    if (!ok || e != cudaSuccess) {
+      if (g2) cudaGraphDestroy(g2);
+      ok = false;
+    } else {
+      graph = g2;
+    }
+  }
+  cudaGetLastError();   // clear any capture error state
+  op->st = user_st;
+  if (!ok) {              // fall back to live V-cycles for this op
+    op->bytes = bsave;
+    for (int l = 0; l < 4; ++l) op->mv[l] = msave[l];
+    g_launches = l0;
+    op->graphs_off = true;
+    return;
+  }
+  helm_op::VGraph vg{};
+  vg.adj = adj; vg.nrhs = nrhs; vg.nact = op->nact;
+  vg.bytes = op->bytes[r0] - b0;
+  for (int l = 0; l < 4; ++l) vg.mv[l] = op->mv[l][r0] - m0[l];
+  vg.launches = g_launches - l0;
+  op->bytes = bsave;
+  for (int l = 0; l < 4; ++l) op->mv[l] = msave[l];
+  g_launches = l0;
+  const cudaError_t e = cudaGraphInstantiate(&vg.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CK(e);
+  op->vgraphs.push_back(vg);
+}
+
 // ------------------------------------------------------------------------------ solve
 // Outer FGMRES(k_inner) in complex128 against the fp64 operator (D15), restarted until the
 // TRUE relative residual of every RHS is <= rtol (R23); converged RHS are masked out.
@@ -978,12 +1065,13 @@ void solve_c128(helm_op* op, int adj, int nrhs, const double2* B, double2* X, co
     if (op->dtype == HELM_C128) {
       M = [op, adj, nrhs](const double2* v, const double* vs, const int* kact, int j, double2* z) {
         launch_copy_scale<double2, double2>(op, 0, nrhs, v, op->w64[0].VB, vs, kact, j);
-        vcycle<double>(op, 0, adj, nrhs, op->w64[0].VB, z);
+        vcycle0_graph<double>(op, adj, nrhs, op->w64[0].VB, op->w64[0].VX);
+        launch_copy_scale<double2, double2>(op, 0, nrhs, op->w64[0].VX, z, nullptr, nullptr, 0);
       };
     } else {
       M = [op, adj, nrhs](const double2* v, const double* vs, const int* kact, int j, double2* z) {
         launch_copy_scale<double2, float2>(op, 0, nrhs, v, op->w32[0].VB, vs, kact, j);
-        vcycle<float>(op, 0, adj, nrhs, op->w32[0].VB, op->w32[0].VX);
+        vcycle0_graph<float>(op, adj, nrhs, op->w32[0].VB, op->w32[0].VX);
         launch_copy_scale<float2, double2>(op, 0, nrhs, op->w32[0].VX, z, nullptr, nullptr, 0);
       };
     }

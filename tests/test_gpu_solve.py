@@ -112,3 +112,20 @@ def test_workspace_within_paper_bound():
     p = synth.cfg3()
     op, w, pml = _setup(p)
     assert op.workspace_vectors() <= 26
+
+
+@pytest.mark.parametrize("make", [synth.tiny2d, synth.tiny3d])
+def test_solves_are_bitwise_reproducible(make):
+    """R30: every reduction is fixed-order fp64 and the level-0 V-cycle replays a captured
+    CUDA graph after its first live run — repeated solves give bitwise identical results."""
+    p = make()
+    op, w, pml = _setup(p, nrhs=len(p.src))
+    Q = fwi.source_matrix(p, w, p.src)
+    b = to_dev(np.ascontiguousarray(Q.T))
+    xs = []
+    for _ in range(3):
+        x = torch.zeros_like(b)
+        rep = api.helm_solve(op, b, x)
+        assert all(r["converged"] for r in rep)
+        xs.append(to_host(x))
+    assert np.array_equal(xs[0], xs[1]) and np.array_equal(xs[1], xs[2])
