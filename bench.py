@@ -272,7 +272,8 @@ def matvec_probe(dtype_name="c128", N=256, nrhs=1, reps=10):
     from paper_1703_09268_b200 import api
     p = synth.cfg5(N)
     dtype = api.C128 if dtype_name == "c128" else api.C64
-    op = api.helm_setup(api.Grid.of(p), p.m, 2 * np.pi * 6.0, api.Pml(v_ref=4500.0), dtype, max_rhs=nrhs)
+    op = api.helm_setup(api.Grid.of(p), p.m, 2 * np.pi * 6.0, api.Pml(v_ref=4500.0), dtype, max_rhs=nrhs,
+                        mlopts=api.MlOpts(levels=0))   # operator only: no solver workspace
     td = torch.complex128 if dtype == api.C128 else torch.complex64
     g = torch.Generator(device="cuda").manual_seed(1)
     n_ext = p.n_ext
@@ -389,7 +390,8 @@ def main():
     if rank == 0:
         if size == 1 and not args.no_matvec:
             out["matvec"] = {k: matvec_probe(*k_) for k, k_ in
-                             (("c128_b1", ("c128", 256, 1)), ("c64_b4", ("c64", 256, 4)))}
+                             (("c128_b1_256", ("c128", 256, 1)), ("c128_b1_512", ("c128", 512, 1)),
+                              ("c128_b4_256", ("c128", 256, 4)), ("c64_b4_256", ("c64", 256, 4)))}
         if size == 1 and not args.no_cpu_baseline:
             from oracle import discretize as D
             out["cpu_baseline"] = cpu_baseline(prob, D.PmlParams(v_ref=3000.0))

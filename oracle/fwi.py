@@ -82,6 +82,61 @@ def misfit_grad(prob, pml: PmlParams, d_obs: np.ndarray, m_int=None, src_ids=Non
     return f, g.reshape(prob.m.shape)
 
 
+# ----------------------------------------------------------------------------- SURVEY §8(f) rank 1
+# Linearised modelling, its adjoint and the Gauss-Newton Hessian (Table 1, Table 2
+# P:111-117; Listing 1 JACOBI_FORW / JACOBI_ADJ / HESS_GN P:167-180). With A = I (STD2, Eq. 7):
+#   T dm  = DH(m)[dm] u = omega^2 u (.) (E dm)
+#   T^* z = E^T Re(omega^2 conj(u) (.) z)     (sum_srcs = to_phys * real)
+#   J dm  = P_r Du[dm],  Du[dm] = -H^-1 T dm
+#   J^H y = T^* H^-H (-P_r^T y)
+#   H_GN dm = J^H J dm = T^* H^-H (-P_r^T P_r (-H^-1 T dm))
+# (Listing 1 writes T(U)*dU in HESS_GN where Table 1 has T^*: the adjoint is used.)
+
+def jacobian(prob, pml: PmlParams, dm: np.ndarray, m_int=None, src_ids=None, weights=None) -> np.ndarray:
+    """Listing 1 JACOBI_FORW: d_lin[f, s, k] = (P_r (-H^-1 T dm))_k, shape (nfreq, nsrc, nrec)."""
+    src_ids = prob.src if src_ids is None else src_ids
+    dm_ext = extension_matrix(prob) @ np.asarray(dm, np.float64).ravel()
+    out = []
+    for fi, fr in enumerate(prob.freqs):
+        w = 2.0 * np.pi * fr
+        S = 1.0 if weights is None else weights[fi]
+        lu = LU(helmholtz_matrix(prob, w, pml, m_int))
+        U = lu.solve(source_matrix(prob, w, src_ids, S))
+        dU = lu.solve(-(w**2) * U * dm_ext[:, None])
+        out.append(receivers(prob, dU).T)
+    return np.stack(out)
+
+
+def jacobian_adjoint(prob, pml: PmlParams, y: np.ndarray, m_int=None, src_ids=None, weights=None) -> np.ndarray:
+    """Listing 1 JACOBI_ADJ: g = E^T sum Re(omega^2 conj(u) H^-H(-P_r^T y)); y: (nfreq, nsrc, nrec)."""
+    src_ids = prob.src if src_ids is None else src_ids
+    g_ext = np.zeros(prob.n_ext)
+    for fi, fr in enumerate(prob.freqs):
+        w = 2.0 * np.pi * fr
+        S = 1.0 if weights is None else weights[fi]
+        lu = LU(helmholtz_matrix(prob, w, pml, m_int))
+        U = lu.solve(source_matrix(prob, w, src_ids, S))
+        V = lu.solve(-receivers_adjoint(prob, y[fi].T), adjoint=True)
+        g_ext += np.sum(np.real(w**2 * np.conj(U) * V), axis=1)
+    return (extension_matrix(prob).T @ g_ext).reshape(prob.m.shape)
+
+
+def gn_hessian(prob, pml: PmlParams, dm: np.ndarray, m_int=None, src_ids=None, weights=None) -> np.ndarray:
+    """Listing 1 HESS_GN (with T^*): three solves per (source, frequency) (Table 2)."""
+    src_ids = prob.src if src_ids is None else src_ids
+    dm_ext = extension_matrix(prob) @ np.asarray(dm, np.float64).ravel()
+    g_ext = np.zeros(prob.n_ext)
+    for fi, fr in enumerate(prob.freqs):
+        w = 2.0 * np.pi * fr
+        S = 1.0 if weights is None else weights[fi]
+        lu = LU(helmholtz_matrix(prob, w, pml, m_int))
+        U = lu.solve(source_matrix(prob, w, src_ids, S))
+        dU = lu.solve(-(w**2) * U * dm_ext[:, None])
+        V = lu.solve(-receivers_adjoint(prob, receivers(prob, dU)), adjoint=True)
+        g_ext += np.sum(np.real(w**2 * np.conj(U) * V), axis=1)
+    return (extension_matrix(prob).T @ g_ext).reshape(prob.m.shape)
+
+
 def taylor_errors(fun, m, dm, g, ts):
     """§6.1: e0(t) = |f(m+t dm) - f(m)|, e1(t) = |f(m+t dm) - f(m) - t <g, dm>|."""
     f0 = fun(m)

@@ -74,3 +74,58 @@ def test_gradient_matches_directional_difference():
     fm = fwi.misfit_grad(p, pml, d, p.m - t * dm)[0]
     fd = (fp - fm) / (2 * t)
     assert abs(fd - np.sum(g * dm)) <= 1e-6 * abs(fd)
+
+
+# ---------------------------------------------------------------- SURVEY §8(f) rank 1 pins
+def _lin_setup():
+    p = synth.tiny2d()
+    pml = D.PmlParams(v_ref=3000.0)
+    rng = np.random.default_rng(2)
+    dm = rng.standard_normal(p.m.shape) * 0.05 * p.m
+    return p, pml, dm
+
+
+def test_jacobian_matches_central_differences_of_forward_modelling():
+    """J dm = dF/dm [dm]: central differences of the (pinned) forward modelling converge to
+    it at second order (an independent check of the linearisation, Table 1 row J)."""
+    p, pml, dm = _lin_setup()
+    J = fwi.jacobian(p, pml, dm)
+    errs = []
+    for t in (1e-2, 5e-3, 2.5e-3):
+        fd = (fwi.forward_data(p, pml, p.m + t * dm) - fwi.forward_data(p, pml, p.m - t * dm)) / (2 * t)
+        errs.append(np.linalg.norm(fd - J) / np.linalg.norm(J))
+    rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert errs[-1] < 1e-4 and np.all(np.abs(rates - 2) < 0.3), (errs, rates)
+
+
+def test_jacobian_adjoint_dot_test():
+    """Table 5: <J dm, y> = <dm, J^H y> (paper: 1.9973e-9 at solver tol 1e-10; LU here)."""
+    p, pml, dm = _lin_setup()
+    rng = np.random.default_rng(5)
+    y = (rng.standard_normal((len(p.freqs), len(p.src), len(p.rec)))
+         + 1j * rng.standard_normal((len(p.freqs), len(p.src), len(p.rec))))
+    lhs = np.real(np.vdot(y, fwi.jacobian(p, pml, dm)))
+    rhs = float(np.sum(dm * fwi.jacobian_adjoint(p, pml, y)))
+    assert abs(lhs - rhs) <= 1e-12 * max(abs(lhs), abs(rhs))
+
+
+def test_jacobian_adjoint_of_residual_is_the_gradient():
+    """grad f = J^H (P u - d) (Table 1: grad f = T^* V, V = -H^-H P^T grad phi)."""
+    p, pml, _ = _lin_setup()
+    d = fwi.forward_data(p, pml, p.m_true)
+    f, g = fwi.misfit_grad(p, pml, d)
+    r = fwi.forward_data(p, pml, p.m) - d
+    assert np.linalg.norm(fwi.jacobian_adjoint(p, pml, r) - g) <= 1e-12 * np.linalg.norm(g)
+
+
+def test_gauss_newton_is_jh_j_symmetric_psd():
+    """H_GN dm = J^H J dm (Table 1), three solves per pair (Table 2); symmetric, PSD."""
+    p, pml, dm = _lin_setup()
+    dm2 = np.random.default_rng(7).standard_normal(p.m.shape) * 0.05 * p.m
+    Hd = fwi.gn_hessian(p, pml, dm)
+    assert np.linalg.norm(Hd - fwi.jacobian_adjoint(p, pml, fwi.jacobian(p, pml, dm))) <= 1e-12 * np.linalg.norm(Hd)
+    a = float(np.sum(dm2 * Hd))
+    b = float(np.sum(dm * fwi.gn_hessian(p, pml, dm2)))
+    assert abs(a - b) <= 1e-11 * max(abs(a), abs(b))
+    Jd = fwi.jacobian(p, pml, dm)
+    assert abs(float(np.sum(dm * Hd)) - np.linalg.norm(Jd) ** 2) <= 1e-11 * np.linalg.norm(Jd) ** 2
