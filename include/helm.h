@@ -131,6 +131,45 @@ helm_status fwi_forward(const helm_grid* grid, const double* m_slowness2, int32_
                         helm_dtype dtype, const helm_solve_opts* opts, int32_t max_rhs,
                         double* d_host, helm_solve_report* report_host, void* cuda_stream);
 
+/* ---- the linearised operators of Listing 1 (Table 1) ------
+ * With T dm = omega^2 u (E dm) (the Born source, D2/D5) and T^* z = E^T Re(omega^2 conj(u) z):
+ *   J dm   = P_r du,  du = -H^-1 T dm                    (JACOBI_FORW, 2 solves per pair)
+ *   J^H y  = T^* H^-H(-P_r^T y)                           (JACOBI_ADJ, 2 solves per pair)
+ *   GN dm  = J^H J dm = T^* H^-H(-P_r^T P_r du)           (HESS_GN, 3 solves per pair, Table 2)
+ * Same conventions as fwi_misfit_grad (host node ids, host data, joint (source, frequency)
+ * batches of at most max_rhs). dm: host fp64 interior perturbation of m = slowness^2.
+ * Reports: NULL or [nfreq][src_end - src_begin][2] (J, J^H: forward, second solve) or [..][3]
+ * (GN: forward, born, adjoint). Errors as fwi_misfit_grad. */
+
+/* d_host: host complex128 [nfreq][src_end - src_begin][nrec] = J dm for this shard's sources. */
+helm_status fwi_jacobian(const helm_grid* grid, const double* m_slowness2, int32_t nfreq,
+                         const double* freq_hz, const double* src_weight_reim,
+                         int32_t src_begin, int32_t src_end, const int64_t* src_node,
+                         int32_t nrec, const int64_t* rec_node, const double* dm,
+                         const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts,
+                         int32_t max_rhs, double* d_host, helm_solve_report* report_host,
+                         void* cuda_stream);
+
+/* y_reim: host complex128 [nfreq][nsrc_total][nrec] (the whole survey; this shard reads
+ * its own sources). g_dev: device fp64 [n_interior] = this shard's part of J^H y (all-reduce
+ * across shards is the caller's). */
+helm_status fwi_jacobian_adjoint(const helm_grid* grid, const double* m_slowness2, int32_t nfreq,
+                                 const double* freq_hz, const double* src_weight_reim,
+                                 int32_t nsrc_total, int32_t src_begin, int32_t src_end,
+                                 const int64_t* src_node, int32_t nrec, const int64_t* rec_node,
+                                 const double* y_reim, const helm_pml* pml, helm_dtype dtype,
+                                 const helm_solve_opts* opts, int32_t max_rhs, double* g_dev,
+                                 helm_solve_report* report_host, void* cuda_stream);
+
+/* h_dev: device fp64 [n_interior] = this shard's part of J^H J dm. */
+helm_status fwi_gn_hessian(const helm_grid* grid, const double* m_slowness2, int32_t nfreq,
+                           const double* freq_hz, const double* src_weight_reim,
+                           int32_t src_begin, int32_t src_end, const int64_t* src_node,
+                           int32_t nrec, const int64_t* rec_node, const double* dm,
+                           const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts,
+                           int32_t max_rhs, double* h_dev, helm_solve_report* report_host,
+                           void* cuda_stream);
+
 /* ---- inspection entry points (same op; used by the parity tests) ---------------------- */
 
 /* Number of levels and per-level extended sizes (x, y, z). dims_host: [levels][3]. */

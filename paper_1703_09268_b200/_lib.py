@@ -63,6 +63,15 @@ SIGNATURES = {
     "fwi_forward": (C.c_int, [C.POINTER(HelmGrid), _d, C.c_int32, _d, _d, C.c_int32, C.c_int32, _i64,
                               C.c_int32, _i64, C.POINTER(HelmPml), C.c_int, C.POINTER(HelmSolveOpts),
                               C.c_int32, _d, _rep, _P]),
+    "fwi_jacobian": (C.c_int, [C.POINTER(HelmGrid), _d, C.c_int32, _d, _d, C.c_int32, C.c_int32, _i64,
+                               C.c_int32, _i64, _d, C.POINTER(HelmPml), C.c_int, C.POINTER(HelmSolveOpts),
+                               C.c_int32, _d, _rep, _P]),
+    "fwi_jacobian_adjoint": (C.c_int, [C.POINTER(HelmGrid), _d, C.c_int32, _d, _d, C.c_int32, C.c_int32,
+                                       C.c_int32, _i64, C.c_int32, _i64, _d, C.POINTER(HelmPml), C.c_int,
+                                       C.POINTER(HelmSolveOpts), C.c_int32, _P, _rep, _P]),
+    "fwi_gn_hessian": (C.c_int, [C.POINTER(HelmGrid), _d, C.c_int32, _d, _d, C.c_int32, C.c_int32, _i64,
+                                 C.c_int32, _i64, _d, C.POINTER(HelmPml), C.c_int, C.POINTER(HelmSolveOpts),
+                                 C.c_int32, _P, _rep, _P]),
     "helm_levels": (C.c_int, [_P, C.POINTER(C.c_int32), _i64]),
     "helm_get_level": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64, _d, _d]),
     "helm_vcycle": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),

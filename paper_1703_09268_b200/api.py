@@ -244,6 +244,79 @@ def fwi_forward(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], src
     return d, [rep[i].as_dict() for i in range(0, nrep, 2)]
 
 
+def _dp(a: np.ndarray):
+    return a.view(np.float64).ctypes.data_as(C.POINTER(C.c_double))
+
+
+def fwi_jacobian(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], src_node: np.ndarray,
+                 rec_node: np.ndarray, dm: np.ndarray, pml: Pml, dtype: int = C128, opts: SolveOpts = SolveOpts(),
+                 max_rhs: int = 16, src_range: Optional[Tuple[int, int]] = None, weights=None, stream=None):
+    """Listing 1 JACOBI_FORW: returns (J dm as (nfreq, ns, nrec) complex128 host, reports [.., 2])."""
+    lib = L.load()
+    m = np.ascontiguousarray(m_slowness2, np.float64)
+    dmv = np.ascontiguousarray(dm, np.float64)
+    src = np.ascontiguousarray(src_node, np.int64)
+    rec = np.ascontiguousarray(rec_node, np.int64)
+    f, w = _freq_args(freqs, weights)
+    s0, s1 = (0, len(src)) if src_range is None else src_range
+    d = np.zeros((len(f), s1 - s0, len(rec)), np.complex128)
+    nrep = len(f) * (s1 - s0) * 2
+    rep = (L.HelmSolveReport * max(nrep, 1))()
+    g, p, so = grid.c(), pml.c(), opts.c()
+    L.check(lib.fwi_jacobian(C.byref(g), _dptr(m), len(f), _dptr(f), None if w is None else _dptr(w), s0, s1,
+                             _i64ptr(src), len(rec), _i64ptr(rec), _dptr(dmv), C.byref(p), dtype, C.byref(so),
+                             max_rhs, _dp(d), rep, _stream(stream)))
+    return d, [rep[i].as_dict() for i in range(nrep)]
+
+
+def fwi_jacobian_adjoint(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], src_node: np.ndarray,
+                         rec_node: np.ndarray, y: np.ndarray, pml: Pml, dtype: int = C128,
+                         opts: SolveOpts = SolveOpts(), max_rhs: int = 16,
+                         src_range: Optional[Tuple[int, int]] = None, weights=None,
+                         out: Optional[torch.Tensor] = None, stream=None):
+    """Listing 1 JACOBI_ADJ: returns (J^H y as fp64 device (n_interior,), reports [.., 2]).
+    y: host complex128 (nfreq, nsrc_total, nrec)."""
+    lib = L.load()
+    m = np.ascontiguousarray(m_slowness2, np.float64)
+    src = np.ascontiguousarray(src_node, np.int64)
+    rec = np.ascontiguousarray(rec_node, np.int64)
+    yv = np.ascontiguousarray(y, np.complex128)
+    f, w = _freq_args(freqs, weights)
+    s0, s1 = (0, len(src)) if src_range is None else src_range
+    if out is None:
+        out = torch.empty(grid.n_interior, dtype=torch.float64, device="cuda")
+    nrep = len(f) * (s1 - s0) * 2
+    rep = (L.HelmSolveReport * max(nrep, 1))()
+    g, p, so = grid.c(), pml.c(), opts.c()
+    L.check(lib.fwi_jacobian_adjoint(C.byref(g), _dptr(m), len(f), _dptr(f), None if w is None else _dptr(w),
+                                     len(src), s0, s1, _i64ptr(src), len(rec), _i64ptr(rec), _dp(yv), C.byref(p),
+                                     dtype, C.byref(so), max_rhs, _tptr(out), rep, _stream(stream)))
+    return out, [rep[i].as_dict() for i in range(nrep)]
+
+
+def fwi_gn_hessian(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], src_node: np.ndarray,
+                   rec_node: np.ndarray, dm: np.ndarray, pml: Pml, dtype: int = C128, opts: SolveOpts = SolveOpts(),
+                   max_rhs: int = 16, src_range: Optional[Tuple[int, int]] = None, weights=None,
+                   out: Optional[torch.Tensor] = None, stream=None):
+    """Listing 1 HESS_GN: returns (J^H J dm as fp64 device (n_interior,), reports [.., 3])."""
+    lib = L.load()
+    m = np.ascontiguousarray(m_slowness2, np.float64)
+    dmv = np.ascontiguousarray(dm, np.float64)
+    src = np.ascontiguousarray(src_node, np.int64)
+    rec = np.ascontiguousarray(rec_node, np.int64)
+    f, w = _freq_args(freqs, weights)
+    s0, s1 = (0, len(src)) if src_range is None else src_range
+    if out is None:
+        out = torch.empty(grid.n_interior, dtype=torch.float64, device="cuda")
+    nrep = len(f) * (s1 - s0) * 3
+    rep = (L.HelmSolveReport * max(nrep, 1))()
+    g, p, so = grid.c(), pml.c(), opts.c()
+    L.check(lib.fwi_gn_hessian(C.byref(g), _dptr(m), len(f), _dptr(f), None if w is None else _dptr(w), s0, s1,
+                               _i64ptr(src), len(rec), _i64ptr(rec), _dptr(dmv), C.byref(p), dtype, C.byref(so),
+                               max_rhs, _tptr(out), rep, _stream(stream)))
+    return out, [rep[i].as_dict() for i in range(nrep)]
+
+
 # ---------------------------------------------------------------------------- measurement
 def profile(enable: bool, stride: int = 1):
     """Sample every `stride`-th launch of each kernel class with CUDA events on its stream."""

@@ -1181,29 +1181,55 @@ std::vector<long long> to_ext(const helm_grid& G, const int64_t* ids, int n) {
   return e;
 }
 
-// Listing 1 `case OBJ` / FORW_MODEL over this rank's (frequency, source) pairs. The pairs
-// are processed in joint batches of up to max_rhs right-hand sides (frequency-major order):
-// each batch is ONE batched forward solve and ONE batched adjoint solve whose RHS may use
-// different frequencies (per-RHS operator tables, Geo::rop) — the paper's data parallelism
-// over the joint (source, frequency) index set (Fig. 2) inside one GPU.
+// Listing 1's PDEfunc modes over this rank's (frequency, source) pairs:
+//   OBJ     f = sum 1/2 |P_r u - d|^2 and g = T^* V (2 solves per pair)
+//   FORW    d = P_r u (1 solve)
+//   JAC     d_lin = P_r Du[dm], Du[dm] = -H^-1 T dm (2 solves)
+//   JACADJ  g = T^* H^-H (-P_r^T y) (2 solves)
+//   GN      g = T^* H^-H (-P_r^T P_r Du[dm]) (3 solves, Table 2)
+// The pairs are processed in joint batches of up to max_rhs right-hand sides (frequency-major
+// order): each batch is ONE batched solve per stage whose RHS may use different frequencies
+// (per-RHS operator tables, Geo::rop) — the paper's data parallelism over the joint (source,
+// frequency) index set (Fig. 2) inside one GPU.
+enum FwiMode { FW_OBJ = 0, FW_FORW, FW_JAC, FW_JACADJ, FW_GN };
+
 template <typename R>
-void fwi_run(helm_op* op, const helm_grid& G, int nfreq, const double* freq, const double* sw, int nsrc_total,
-             int s_begin, int s_end, const int64_t* src, int nrec, const int64_t* rec, const double* dobs,
-             const helm_solve_opts& so, double* fg, helm_solve_report* rep, double* d_out, cudaStream_t st) {
+void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const double* freq, const double* sw,
+             int nsrc_total, int s_begin, int s_end, const int64_t* src, int nrec, const int64_t* rec,
+             const double* dobs /* OBJ: d_obs, JACADJ: y; host [nfreq][nsrc_total][nrec] */,
+             const double* dm /* JAC, GN: host interior */, const helm_solve_opts& so, double* out /* OBJ: [f|g],
+             JACADJ/GN: g */, helm_solve_report* rep, double* d_out /* FORW, JAC: host [nfreq][ns][nrec] */,
+             cudaStream_t st) {
   using C = cx<R>;
   FwiBufs fb;
   const long long N = op->lev[0].N;
   const int B = op->max_rhs;
   const int ns = s_end - s_begin;
+  const bool grad = mode == FW_OBJ || mode == FW_JACADJ || mode == FW_GN;
+  const bool born = mode == FW_JAC || mode == FW_GN;
+  const int rs = mode == FW_GN ? 3 : 2;   // report stride per pair
   fb.U = dalloc<C>(fb.keep, (size_t)N * B);
   fb.Bq = dalloc<C>(fb.keep, (size_t)N * B);
-  if (!d_out) {
+  void* dU = born ? dalloc<C>(fb.keep, (size_t)N * B) : nullptr;
+  if (grad) {
     fb.V = dalloc<C>(fb.keep, (size_t)N * B);
     fb.A = dalloc<C>(fb.keep, (size_t)N * B);
     fb.gext = dalloc<double>(fb.keep, N);
     fb.f = dalloc<double>(fb.keep, 1);
     CK(cudaMemsetAsync(fb.gext, 0, sizeof(double) * N, st));
     CK(cudaMemsetAsync(fb.f, 0, sizeof(double), st));
+  }
+  double* dm_ext = nullptr;
+  if (born) {   // dm_ext = E dm (D2)
+    const long long nint = G.n[0] * G.n[1] * G.n[2];
+    double* dm_int = dalloc<double>(fb.keep, nint);
+    dm_ext = dalloc<double>(fb.keep, N);
+    CK(cudaMemcpyAsync(dm_int, dm, sizeof(double) * nint, cudaMemcpyHostToDevice, st));
+    const LevelDev& L0 = op->lev[0];
+    prof_count(KC_FWI);
+    k_extend<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(L0.nx, L0.ny, L0.nz, (int)G.n[0], (int)G.n[1], (int)G.n[2],
+                                                          G.pml[0][0], G.pml[1][0], G.pml[2][0], dm_int, dm_ext);
+    CKL();
   }
   fb.d = dalloc<double2>(fb.keep, (size_t)B * std::max(nrec, 1));
   double2* amp_d = dalloc<double2>(fb.keep, B);
@@ -1224,6 +1250,21 @@ void fwi_run(helm_op* op, const helm_grid& G, int nfreq, const double* freq, con
   std::vector<long long> srcb_h(B);
   std::vector<int> rop_h(B), fi_h(B), si_h(B);
   const long long npairs = (long long)nfreq * ns;
+  auto put_rep = [&](int nb, int k) {
+    if (rep)
+      for (int b = 0; b < nb; ++b) rep[((size_t)fi_h[b] * ns + si_h[b]) * rs + k] = rtmp[b];
+  };
+  auto gather_out = [&](int nb, const void* Ufield) {   // d_out[f][s][:] = P_r field
+    if (!nrec) return;
+    prof_count(KC_FWI);
+    k_gather_data<R><<<(unsigned)((nb * (long long)nrec + 255) / 256), 256, 0, st>>>(nb, nrec, N, fb.rec_ext,
+                                                                                (const C*)Ufield, fb.d);
+    CKL();
+    CK(cudaMemcpyAsync(dbat.data(), fb.d, sizeof(double2) * nb * nrec, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < nb; ++b)
+      std::memcpy(d_out + 2 * (((size_t)fi_h[b] * ns + si_h[b]) * nrec), &dbat[(size_t)b * nrec], sizeof(double2) * nrec);
+  };
   for (long long p0 = 0; p0 < npairs; p0 += B) {
     const int nb = (int)std::min<long long>(B, npairs - p0);
     // the batch's operators (distinct frequencies, in order) and per-RHS data
@@ -1251,50 +1292,54 @@ void fwi_run(helm_op* op, const helm_grid& G, int nfreq, const double* freq, con
     CKL();
     // forward solves u = H^-1 q
     solve_any(op, 0, nb, fb.Bq, fb.U, so, rtmp.data());
-    for (int b = 0; b < nb; ++b)
-      if (rep) rep[((size_t)fi_h[b] * ns + si_h[b]) * 2 + 0] = rtmp[b];
-    if (d_out) {   // FORW_MODEL: d = P_r u
-      if (nrec) {
-        prof_count(KC_FWI);
-        k_gather_data<R><<<(unsigned)((nb * (long long)nrec + 255) / 256), 256, 0, st>>>(nb, nrec, N, fb.rec_ext,
-                                                                                    (const C*)fb.U, fb.d);
-        CKL();
-        CK(cudaMemcpyAsync(dbat.data(), fb.d, sizeof(double2) * nb * nrec, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        for (int b = 0; b < nb; ++b)
-          std::memcpy(d_out + 2 * (((size_t)fi_h[b] * ns + si_h[b]) * nrec), &dbat[(size_t)b * nrec],
-                      sizeof(double2) * nrec);
-      }
-      continue;
+    put_rep(nb, 0);
+    if (mode == FW_FORW) { gather_out(nb, fb.U); continue; }
+    if (born) {   // Du[dm] = -H^-1 T dm
+      prof_count(KC_FWI);
+      k_born_src<R><<<TARGET_BLOCKS, 256, 0, st>>>(nb, N, w2_d, (const C*)fb.U, dm_ext, (C*)fb.Bq);
+      CKL();
+      solve_any(op, 0, nb, fb.Bq, dU, so, rtmp.data());
+      put_rep(nb, 1);
+      if (mode == FW_JAC) { gather_out(nb, dU); continue; }
     }
-    // a7: r = P_r u - d, f += 1/2 |r|^2, adjoint source -P_r^T r
-    for (int b = 0; b < nb; ++b)
-      std::memcpy(&dbat[(size_t)b * nrec], dobs + 2 * (((size_t)fi_h[b] * nsrc_total + s_begin + si_h[b]) * nrec),
-                  sizeof(double2) * nrec);
-    if (nrec) CK(cudaMemcpyAsync(fb.d, dbat.data(), sizeof(double2) * nb * nrec, cudaMemcpyHostToDevice, st));
+    // adjoint source: OBJ: -P_r^T (P_r u - d) (+ f); JACADJ: -P_r^T y; GN: -P_r^T P_r Du[dm]
+    if (mode != FW_GN && nrec) {
+      for (int b = 0; b < nb; ++b)
+        std::memcpy(&dbat[(size_t)b * nrec], dobs + 2 * (((size_t)fi_h[b] * nsrc_total + s_begin + si_h[b]) * nrec),
+                    sizeof(double2) * nrec);
+      CK(cudaMemcpyAsync(fb.d, dbat.data(), sizeof(double2) * nb * nrec, cudaMemcpyHostToDevice, st));
+    }
     CK(cudaMemsetAsync(fb.A, 0, sizeof(C) * N * nb, st));
-    dim3 gg(std::max(1, std::min(TARGET_BLOCKS, (nb * nrec + 255) / 256)));
-    prof_count(KC_FWI);
-    k_gather_residual<R><<<gg, HELM_RED_THREADS, 0, st>>>(nb, nrec, N, fb.rec_ext, fb.d, (const C*)fb.U, (C*)fb.A,
-                                                            fb.f, op->rb);
-    CKL();
-    // a8: adjoint solves v = H^-H(-P_r^T r)
+    if (nrec) {
+      if (mode == FW_JACADJ) {
+        prof_count(KC_FWI);
+        k_scatter_neg<R><<<(unsigned)((nb * (long long)nrec + 255) / 256), 256, 0, st>>>(nb, nrec, N, fb.rec_ext, fb.d,
+                                                                                    (C*)fb.A);
+        CKL();
+      } else {
+        if (mode == FW_GN) CK(cudaMemsetAsync(fb.d, 0, sizeof(double2) * nb * nrec, st));   // "data" = 0
+        dim3 gg(std::max(1, std::min(TARGET_BLOCKS, (nb * nrec + 255) / 256)));
+        prof_count(KC_FWI);
+        k_gather_residual<R><<<gg, HELM_RED_THREADS, 0, st>>>(nb, nrec, N, fb.rec_ext, fb.d,
+                                                                (const C*)(mode == FW_GN ? dU : fb.U), (C*)fb.A, fb.f,
+                                                                op->rb);
+        CKL();
+      }
+    }
+    // a8: adjoint solves
     solve_any(op, 1, nb, fb.A, fb.V, so, rtmp.data());
-    for (int b = 0; b < nb; ++b)
-      if (rep) rep[((size_t)fi_h[b] * ns + si_h[b]) * 2 + 1] = rtmp[b];
+    put_rep(nb, rs - 1);
     // a9: g_ext += sum_b Re(omega_b^2 conj(u_b) v_b)
     prof_count(KC_FWI);
     k_grad<R><<<blas_blocks(N, 1), 256, 0, st>>>(nb, N, w2_d, (const C*)fb.U, (const C*)fb.V, fb.gext);
     CKL();
   }
-  // the host staging buffers above are reused across batches: make sure the last copies
-  // are done before they go out of scope
-  if (!d_out) {
+  if (grad) {
     const long long nint = G.n[0] * G.n[1] * G.n[2];
     prof_count(KC_FWI);
     k_fold<<<(unsigned)((nint + 255) / 256), 256, 0, st>>>(op->lev[0].nx, op->lev[0].ny, op->lev[0].nz, (int)G.n[0],
                                                            (int)G.n[1], (int)G.n[2], G.pml[0][0], G.pml[1][0],
-                                                           G.pml[2][0], fb.gext, fb.f, fg);
+                                                           G.pml[2][0], fb.gext, mode == FW_OBJ ? fb.f : nullptr, out);
     CKL();
   }
   CK(cudaStreamSynchronize(st));
@@ -1439,11 +1484,11 @@ helm_status helm_solve(helm_op* op, int32_t adjoint, int32_t nrhs, const void* b
   });
 }
 
-static helm_status fwi_common(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq,
-                              const double* sw, int32_t nsrc_total, int32_t s_begin, int32_t s_end,
+static helm_status fwi_common(FwiMode mode, const helm_grid* grid, const double* m, int32_t nfreq,
+                              const double* freq, const double* sw, int32_t nsrc_total, int32_t s_begin, int32_t s_end,
                               const int64_t* src, int32_t nrec, const int64_t* rec, const double* dobs,
-                              const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts, int32_t max_rhs,
-                              double* fg, helm_solve_report* rep, double* d_out, void* stream) {
+                              const double* dm, const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts,
+                              int32_t max_rhs, double* out, helm_solve_report* rep, double* d_out, void* stream) {
   return wrap([&] {
     validate_grid(grid);
     REQ(m && freq && src && pml, HELM_ERR_ARG, "NULL argument");
@@ -1453,20 +1498,27 @@ static helm_status fwi_common(const helm_grid* grid, const double* m, int32_t nf
     REQ(0 <= s_begin && s_begin <= s_end && s_end <= nsrc_total, HELM_ERR_ARG, "bad source range");
     REQ(nrec >= 0 && (nrec == 0 || rec), HELM_ERR_ARG, "bad receivers");
     REQ(max_rhs >= 1, HELM_ERR_ARG, "max_rhs must be >= 1");
-    if (!d_out) REQ(fg && (dobs || nrec == 0), HELM_ERR_ARG, "fg / d_obs NULL");
+    if (mode == FW_OBJ || mode == FW_JACADJ) REQ(out && (dobs || nrec == 0), HELM_ERR_ARG, "output / data NULL");
+    if (mode == FW_GN) REQ(out && dm, HELM_ERR_ARG, "output / dm NULL");
+    if (mode == FW_JAC) REQ(d_out && dm, HELM_ERR_ARG, "d_out / dm NULL");
+    if (mode == FW_FORW) REQ(d_out, HELM_ERR_ARG, "d_out NULL");
     const cudaStream_t st = (cudaStream_t)stream;
     helm_op* op = fwi_op(grid, m, 2.0 * M_PI * freq[0], pml, dtype, max_rhs, st);
     helm_solve_opts so = opts ? *opts : default_solve_opts(op);
     check_solve_opts(op, so);
-    if (s_end == s_begin) {   // empty shard: f = 0, g = 0
-      if (!d_out) CK(cudaMemsetAsync(fg, 0, sizeof(double) * (1 + grid->n[0] * grid->n[1] * grid->n[2]), st));
+    const long long nint = grid->n[0] * grid->n[1] * grid->n[2];
+    if (s_end == s_begin) {   // empty shard: zero outputs
+      if (mode == FW_OBJ) CK(cudaMemsetAsync(out, 0, sizeof(double) * (1 + nint), st));
+      if (mode == FW_JACADJ || mode == FW_GN) CK(cudaMemsetAsync(out, 0, sizeof(double) * nint, st));
       CK(cudaStreamSynchronize(st));
       return;
     }
     if (dtype == HELM_C128)
-      fwi_run<double>(op, *grid, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, so, fg, rep, d_out, st);
+      fwi_run<double>(op, *grid, mode, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, dm, so, out,
+                      rep, d_out, st);
     else
-      fwi_run<float>(op, *grid, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, so, fg, rep, d_out, st);
+      fwi_run<float>(op, *grid, mode, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, dm, so, out,
+                     rep, d_out, st);
   });
 }
 
@@ -1475,8 +1527,8 @@ helm_status fwi_misfit_grad(const helm_grid* grid, const double* m, int32_t nfre
                             int32_t nrec, const int64_t* rec, const double* dobs, const helm_pml* pml,
                             helm_dtype dtype, const helm_solve_opts* opts, int32_t max_rhs, double* fg,
                             helm_solve_report* rep, void* stream) {
-  return fwi_common(grid, m, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, pml, dtype, opts,
-                    max_rhs, fg, rep, nullptr, stream);
+  return fwi_common(FW_OBJ, grid, m, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, nullptr, pml,
+                    dtype, opts, max_rhs, fg, rep, nullptr, stream);
 }
 
 helm_status fwi_forward(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq, const double* sw,
@@ -1484,8 +1536,34 @@ helm_status fwi_forward(const helm_grid* grid, const double* m, int32_t nfreq, c
                         const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts, int32_t max_rhs,
                         double* d_host, helm_solve_report* rep, void* stream) {
   if (!d_host) { g_err = "d_host is NULL"; return HELM_ERR_ARG; }
-  return fwi_common(grid, m, nfreq, freq, sw, s_end, s_begin, s_end, src, nrec, rec, nullptr, pml, dtype, opts,
-                    max_rhs, nullptr, rep, d_host, stream);
+  return fwi_common(FW_FORW, grid, m, nfreq, freq, sw, s_end, s_begin, s_end, src, nrec, rec, nullptr, nullptr, pml,
+                    dtype, opts, max_rhs, nullptr, rep, d_host, stream);
+}
+
+helm_status fwi_jacobian(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq, const double* sw,
+                         int32_t s_begin, int32_t s_end, const int64_t* src, int32_t nrec, const int64_t* rec,
+                         const double* dm, const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts,
+                         int32_t max_rhs, double* d_host, helm_solve_report* rep, void* stream) {
+  if (!d_host || !dm) { g_err = "d_host / dm is NULL"; return HELM_ERR_ARG; }
+  return fwi_common(FW_JAC, grid, m, nfreq, freq, sw, s_end, s_begin, s_end, src, nrec, rec, nullptr, dm, pml, dtype,
+                    opts, max_rhs, nullptr, rep, d_host, stream);
+}
+
+helm_status fwi_jacobian_adjoint(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq,
+                                 const double* sw, int32_t nsrc_total, int32_t s_begin, int32_t s_end,
+                                 const int64_t* src, int32_t nrec, const int64_t* rec, const double* y,
+                                 const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts, int32_t max_rhs,
+                                 double* g_dev, helm_solve_report* rep, void* stream) {
+  return fwi_common(FW_JACADJ, grid, m, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, y, nullptr, pml,
+                    dtype, opts, max_rhs, g_dev, rep, nullptr, stream);
+}
+
+helm_status fwi_gn_hessian(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq, const double* sw,
+                           int32_t s_begin, int32_t s_end, const int64_t* src, int32_t nrec, const int64_t* rec,
+                           const double* dm, const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts,
+                           int32_t max_rhs, double* h_dev, helm_solve_report* rep, void* stream) {
+  return fwi_common(FW_GN, grid, m, nfreq, freq, sw, s_end, s_begin, s_end, src, nrec, rec, nullptr, dm, pml, dtype,
+                    opts, max_rhs, h_dev, rep, nullptr, stream);
 }
 
 helm_status helm_levels(const helm_op* op, int32_t* levels, int64_t* dims) {

@@ -401,10 +401,12 @@ __global__ void k_grad(int ns, long long N, const double* __restrict__ w2, const
 
 // g = E^T g_ext (D12, R11): each interior cell sums the extended nodes that replicate it
 // (its PML line / face / corner box); written into fg[1 + i]; fg[0] = f.
+// (f == null: model-space output only, g[p] = (E^T g_ext)_p without the leading f slot)
 __global__ void k_fold(int Nx, int Ny, int Nz, int nx, int ny, int nz, int wx, int wy, int wz,
                        const double* __restrict__ gext, const double* __restrict__ f, double* __restrict__ fg) {
   long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p == 0) fg[0] = *f;
+  if (f && p == 0) fg[0] = *f;
+  const int off = f ? 1 : 0;
   if (p >= (long long)nx * ny * nz) return;
   const int ix = p % nx, iy = (p / nx) % ny, iz = p / ((long long)nx * ny);
   auto range = [](int i, int n, int w, int Nn, int& a, int& b) {
@@ -419,7 +421,33 @@ __global__ void k_fold(int Nx, int Ny, int Nz, int nx, int ny, int nz, int wx, i
   for (int k = za; k <= zb; ++k)
     for (int j = ya; j <= yb; ++j)
       for (int i = xa; i <= xb; ++i) s += gext[((long long)k * Ny + j) * Nx + i];
-  fg[1 + p] = s;
+  fg[off + p] = s;
+}
+
+// Born source of the linearised modelling (Table 1 T dm, Eq. 7 with A = I; Listing 1
+// JACOBI_FORW / HESS_GN): B_s = -T dm = -omega_s^2 u_s (.) (E dm), dm_ext = E dm in fp64.
+template <typename R>
+__global__ void k_born_src(int ns, long long N, const double* __restrict__ w2, const cx<R>* __restrict__ U,
+                           const double* __restrict__ dm_ext, cx<R>* __restrict__ B) {
+  const long long tot = (long long)ns * N;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < tot; q += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(q / N);
+    const long long p = q - (long long)s * N;
+    const double2 u = to_d(U[q]);
+    const double c = -w2[s] * dm_ext[p];
+    B[q] = from_d<cx<R>>(make_double2(c * u.x, c * u.y));
+  }
+}
+
+// Adjoint source from host data y (Listing 1 JACOBI_ADJ): A_s = -P_r^T y_s (receivers distinct; A zeroed).
+template <typename R>
+__global__ void k_scatter_neg(int ns, int nrec, long long N, const long long* __restrict__ rec_ext,
+                              const double2* __restrict__ y, cx<R>* __restrict__ A) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)ns * nrec) return;
+  const int s = (int)(q / nrec), k = (int)(q % nrec);
+  const double2 v = y[q];
+  A[(long long)s * N + rec_ext[k]] = from_d<cx<R>>(make_double2(-v.x, -v.y));
 }
 
 // ================================================================= a3/a4 BLAS-1, templated

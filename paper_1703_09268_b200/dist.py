@@ -38,3 +38,38 @@ def misfit_grad_sharded(evaluate: Optional[Callable] = None, nsrc: int = 0, grou
     if size > 1:
         dist.all_reduce(fg, op=dist.ReduceOp.SUM, group=group)
     return fg, rep, (s0, s1)
+
+
+def _reduce_sharded(evaluate: Callable, nsrc: int, group=None, **kw):
+    rank, size = world()
+    s0, s1 = shard(nsrc, rank, size)
+    out, rep = evaluate(src_range=(s0, s1), **kw)
+    if size > 1:
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out, rep, (s0, s1)
+
+
+def jacobian_adjoint_sharded(evaluate: Optional[Callable] = None, nsrc: int = 0, group=None, **kw):
+    """J^H y (Listing 1 JACOBI_ADJ) summed over source shards: same sharding and ONE all-reduce
+    as misfit_grad_sharded; y holds the whole survey, each rank reads its sources."""
+    if evaluate is None:
+        from .api import fwi_jacobian_adjoint as evaluate
+    return _reduce_sharded(evaluate, nsrc, group, **kw)
+
+
+def gn_hessian_sharded(evaluate: Optional[Callable] = None, nsrc: int = 0, group=None, **kw):
+    """J^H J dm (Listing 1 HESS_GN) summed over source shards with ONE all-reduce."""
+    if evaluate is None:
+        from .api import fwi_gn_hessian as evaluate
+    return _reduce_sharded(evaluate, nsrc, group, **kw)
+
+
+def jacobian_sharded(evaluate: Optional[Callable] = None, nsrc: int = 0, **kw):
+    """J dm (Listing 1 JACOBI_FORW) for this rank's sources: data-parallel with no collective —
+    each rank's d_lin[:, s0:s1] is its own output (the caller gathers if it needs the whole)."""
+    if evaluate is None:
+        from .api import fwi_jacobian as evaluate
+    rank, size = world()
+    s0, s1 = shard(nsrc, rank, size)
+    d, rep = evaluate(src_range=(s0, s1), **kw)
+    return d, rep, (s0, s1)
