@@ -136,6 +136,13 @@ struct LevelDev {
   float2* t32[2][3][3] = {};
   double2* z64[2] = {};         // packed z coefficients per adjoint (k_zpack)
   float2* z32[2] = {};
+  // 3D only, for the TMA plane stages: z coefficients padded to 4 per plane, and m with its
+  // row pitch nxq rounded up to a 16-B multiple
+  double2* zq64[2] = {};
+  float2* zq32[2] = {};
+  double* mq64 = nullptr;
+  float* mq32 = nullptr;
+  int nxq = 0;
   int tiles = 0;
 };
 
@@ -312,16 +319,19 @@ template <int N = 0, typename F> void dispatch_k0(int k, F&& f) {
 // HELM_PLANE_OCC / HELM_PLANE_S override, for tuning).
 template <int MODE, bool YC> constexpr int plane_py() { return (YC && MODE < 3) ? 2 : 1; }
 
+// Ring depth S = smem budget / (occupancy target x stage bytes). Measured on the cfg5 matvec
+// (profiles/r01/matvec_occ_ab.txt): complex64 stages are half the bytes, and its kernels are
+// issue-latency bound, so it wants more resident CTAs (8) over a deeper ring; complex128 4.
 struct PlaneTune { int occ_target, s_fixed; };
-const PlaneTune& plane_tune() {
-  static const PlaneTune t{std::max(1, env_int("HELM_PLANE_OCC", 4)), env_int("HELM_PLANE_S", 0)};
+template <typename R> const PlaneTune& plane_tune() {
+  static const PlaneTune t{std::max(1, env_int("HELM_PLANE_OCC", sizeof(R) == 4 ? 8 : 4)), env_int("HELM_PLANE_S", 0)};
   return t;
 }
 
-// TMA tensor map of a batched complex vector [rhs][z][y][x] viewed as reals (x fastest:
-// 2 nx reals per row), box = the 34 x 10 halo'd tile (x0-1 .. x0+32, y0-1 .. y0+8) of one
-// plane of one RHS. Needs 16-B aligned base and row pitch (always for complex128). Returns
-// false when TMA is not used for the array.
+// TMA tensor map of a batched complex vector [rhs][z][y][x] viewed as 8-byte words (x
+// fastest), box = the 34 x 10 halo'd tile (x0-1 .. x0+32, y0-1 .. y0+8) of one plane of one
+// RHS. Needs a 16-B aligned base and row pitch (always for complex128; even nx for
+// complex64). Returns false when TMA is not used for the array.
 PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
@@ -337,22 +347,57 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
 template <typename R>
 bool make_tile_map(CUtensorMap* m, const void* base, int nx, int ny, int nz, int nrhs) {
   auto enc = tma_encoder();
-  // complex128 only: the FLOAT32 (complex64) maps faulted with an illegal instruction on
-  // B200 in this build; complex64 keeps the per-thread cp.async halo path
-  if (sizeof(R) != 8) return false;
   if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
-  const cuuint64_t eb = sizeof(R);
-  if ((2 * (cuuint64_t)nx * eb) % 16) return false;
-  cuuint64_t dims[4] = {2 * (cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz, (cuuint64_t)nrhs};
-  cuuint64_t strides[3] = {2 * (cuuint64_t)nx * eb, 2 * (cuuint64_t)nx * ny * eb, 2 * (cuuint64_t)nx * ny * nz * eb};
-  cuuint32_t box[4] = {68, 10, 1, 1};
+  // the tensor element is an 8-byte word (one complex64, or half a complex128): TMA only
+  // moves bytes, and 8-byte elements keep the 16-B row-pitch rule satisfiable for complex64
+  const cuuint64_t ce = sizeof(cx<R>) / 8;
+  if ((ce * (cuuint64_t)nx * 8) % 16) return false;
+  cuuint64_t dims[4] = {ce * (cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz, (cuuint64_t)nrhs};
+  cuuint64_t strides[3] = {ce * (cuuint64_t)nx * 8, ce * (cuuint64_t)nx * ny * 8, ce * (cuuint64_t)nx * ny * nz * 8};
+  // box = the tile plus its x halo, starting 16-B aligned (PlaneSmem::XO): 34 complex128 or
+  // 36 complex64 per row
+  const cuuint32_t xo = (cuuint32_t)(16 / sizeof(cx<R>));
+  cuuint32_t box[4] = {(cuuint32_t)((32 + 2 * xo) * ce), 10, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
-  const CUresult rc = enc(m, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
-                          const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult rc = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return rc == CUDA_SUCCESS;
 }
+
+// TMA maps of the per-plane operands that are not halo'd: m (16-B pitched copy, box = the
+// 32 x 8 own points of a tile) and the padded z-coefficient rows (box = one plane's 4 entries).
+template <typename R>
+bool make_m_map(CUtensorMap* m, const R* mq, int nxq, int ny, int nz) {
+  auto enc = tma_encoder();
+  if (!enc || !mq) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)nxq, (cuuint64_t)ny, (cuuint64_t)nz};
+  cuuint64_t strides[2] = {(cuuint64_t)nxq * sizeof(R), (cuuint64_t)nxq * ny * sizeof(R)};
+  cuuint32_t box[3] = {32, 8, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+             const_cast<R*>(mq), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <typename R>
+bool make_z_map(CUtensorMap* m, const cx<R>* zq, int nz, int nop) {
+  auto enc = tma_encoder();
+  if (!enc || !zq) return false;
+  const cuuint64_t w = 4 * sizeof(cx<R>) / 8;   // 8-byte words per plane row
+  cuuint64_t dims[2] = {w, (cuuint64_t)nz * nop};
+  cuuint64_t strides[1] = {w * 8};
+  cuuint32_t box[2] = {(cuuint32_t)w, 1};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<cx<R>*>(zq), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <typename R> const R* level_mq(const LevelDev& L);
+template <> const double* level_mq<double>(const LevelDev& L) { return L.mq64; }
+template <> const float* level_mq<float>(const LevelDev& L) { return L.mq32; }
+template <typename R> const cx<R>* level_zq(const LevelDev& L, int adj);
+template <> const double2* level_zq<double>(const LevelDev& L, int adj) { return L.zq64[adj]; }
+template <> const float2* level_zq<float>(const LevelDev& L, int adj) { return L.zq32[adj]; }
 
 struct PlaneCfg { int S = 0, occ = 0; size_t smem = 0; };
 
@@ -384,7 +429,7 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
   auto kern = k_plane<R, 32, 8, PY, MODE, NV, YC>;
   static const PlaneCfg cfg = [&] {
     PlaneCfg c;
-    const PlaneTune& t = plane_tune();
+    const PlaneTune& t = plane_tune<R>();
     c.S = t.s_fixed >= 4 ? std::min(t.s_fixed, 12) : (int)std::min<size_t>(12, (220 * 1024) / (t.occ_target * sb));
     c.S = std::max(c.S, 4);
     c.smem = c.S * sb + 8 * c.S;   // ring + one mbarrier per stage (TMA)
@@ -512,6 +557,10 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
     for (int t = 0; t < nxt && ok; ++t)
       ok = make_tile_map<R>(&a.tm[t], t == 0 ? (const void*)x : (const void*)a.V.p[t - 1], a.g.nx, a.g.ny, a.g.nz, nrhs);
     a.tma = ok ? 1 : 0;
+    static const bool tmq_on = env_int("HELM_TMA_MZ", 1) != 0;
+    const LevelDev& Lv = op->lev[l];
+    a.tmq = a.tma && tmq_on && make_m_map<R>(&a.tmm, level_mq<R>(Lv), Lv.nxq, Lv.ny, Lv.nz) &&
+            make_z_map<R>(&a.tmz, level_zq<R>(Lv, adj), Lv.nz, op->nop);
   }
   const long long units = (long long)a.ntx * a.nty * a.g.nz;
   prof_begin(cls, op->st, l);
@@ -740,6 +789,18 @@ void build_tables(helm_op* op) {
                                                                Lv.t32[adj][2][2], Lv.z32[adj]);
         CKL();
       }
+      if (Lv.ny > 1) {
+        prof_count(KC_SETUP);
+        k_zpack<double2, 4><<<(nzo + 127) / 128, 128, 0, op->st>>>(Lv.nz, op->nop, Lv.t64[adj][2][0],
+                                                                   Lv.t64[adj][2][1], Lv.t64[adj][2][2], Lv.zq64[adj]);
+        CKL();
+        if (op->dtype == HELM_C64) {
+          prof_count(KC_SETUP);
+          k_zpack<float2, 4><<<(nzo + 127) / 128, 128, 0, op->st>>>(Lv.nz, op->nop, Lv.t32[adj][2][0],
+                                                                   Lv.t32[adj][2][1], Lv.t32[adj][2][2], Lv.zq32[adj]);
+          CKL();
+        }
+      }
     }
   }
 }
@@ -766,6 +827,16 @@ void build_models(helm_op* op) {
       k_cast<double, float><<<(unsigned)((Lv.N + 255) / 256), 256, 0, op->st>>>(Lv.N, Lv.m64, Lv.m32);
       CKL();
     }
+  for (int l = 0; l < op->L; ++l) {   // 16-B pitched copies of m for the 3D TMA stages
+    LevelDev& Lv = op->lev[l];
+    if (Lv.ny == 1) continue;
+    const size_t rows = (size_t)Lv.ny * Lv.nz;
+    CK(cudaMemcpy2DAsync(Lv.mq64, sizeof(double) * Lv.nxq, Lv.m64, sizeof(double) * Lv.nx, sizeof(double) * Lv.nx, rows,
+                         cudaMemcpyDeviceToDevice, op->st));
+    if (op->dtype == HELM_C64)
+      CK(cudaMemcpy2DAsync(Lv.mq32, sizeof(float) * Lv.nxq, Lv.m32, sizeof(float) * Lv.nx, sizeof(float) * Lv.nx, rows,
+                           cudaMemcpyDeviceToDevice, op->st));
+  }
 }
 
 template <typename R>
@@ -903,6 +974,15 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
     for (int adj = 0; adj < 2; ++adj) {
       Lv.z64[adj] = dalloc<double2>(op->allocs, (size_t)3 * Lv.nz * HELM_MAXOP);
       if (dtype == HELM_C64) Lv.z32[adj] = dalloc<float2>(op->allocs, (size_t)3 * Lv.nz * HELM_MAXOP);
+      if (Lv.ny > 1) {
+        Lv.zq64[adj] = dalloc<double2>(op->allocs, (size_t)4 * Lv.nz * HELM_MAXOP);
+        if (dtype == HELM_C64) Lv.zq32[adj] = dalloc<float2>(op->allocs, (size_t)4 * Lv.nz * HELM_MAXOP);
+      }
+    }
+    if (Lv.ny > 1) {
+      Lv.nxq = (Lv.nx + 3) / 4 * 4;
+      Lv.mq64 = dalloc<double>(op->allocs, (size_t)Lv.nxq * Lv.ny * Lv.nz);
+      if (dtype == HELM_C64) Lv.mq32 = dalloc<float>(op->allocs, (size_t)Lv.nxq * Lv.ny * Lv.nz);
     }
   }
   op->m_int_d = dalloc<double>(op->allocs, n_int);

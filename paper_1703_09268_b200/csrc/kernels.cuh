@@ -211,8 +211,9 @@ __global__ void k_cast(long long n, const Tin* __restrict__ a, Tout* __restrict_
   long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p < n) b[p] = (Tout)a[p];
 }
-// zpk[(o nz + z) 3 + {0,1,2}] = (lo_z (0 at z = 0), dg_z, up_z (0 at z = nz-1)) of operator o
-template <typename T>
+// zpk[(o nz + z) ZS + {0,1,2}] = (lo_z (0 at z = 0), dg_z, up_z (0 at z = nz-1)) of operator o;
+// ZS = 4 pads each entry with a zero (the 3D TMA copy moves whole 16-B multiples per plane)
+template <typename T, int ZS = 3>
 __global__ void k_zpack(int nz, int nop, const T* __restrict__ lo, const T* __restrict__ dg, const T* __restrict__ up,
                         T* __restrict__ zpk) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -220,9 +221,10 @@ __global__ void k_zpack(int nz, int nop, const T* __restrict__ lo, const T* __re
   const int z = e % nz;
   T zero;
   zero.x = 0; zero.y = 0;
-  zpk[3 * e] = z > 0 ? lo[e] : zero;
-  zpk[3 * e + 1] = dg[e];
-  zpk[3 * e + 2] = z < nz - 1 ? up[e] : zero;
+  zpk[ZS * e] = z > 0 ? lo[e] : zero;
+  zpk[ZS * e + 1] = dg[e];
+  zpk[ZS * e + 2] = z < nz - 1 ? up[e] : zero;
+  if constexpr (ZS == 4) zpk[ZS * e + 3] = zero;
 }
 
 __global__ void k_cast_c(long long n, const double2* __restrict__ a, float2* __restrict__ b) {

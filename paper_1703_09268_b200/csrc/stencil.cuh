@@ -54,6 +54,18 @@ __device__ __forceinline__ void tma_load4(unsigned dst, const CUtensorMap* map, 
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma_load3(unsigned dst, const CUtensorMap* map, unsigned bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load2(unsigned dst, const CUtensorMap* map, unsigned bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
 
@@ -99,8 +111,11 @@ template <typename R> struct PlaneArgs {
   int cpg;                 // CTAs per group
   int nzc, zlen;           // z-chunks per tile and their length
   int S;                   // ring stages (>= 4)
-  int tma;                 // halo'd tiles by TMA (tm[0] = x / W, tm[1 + i] = V_i) instead of cp.async
+  int tma;                 // TMA stages (tm[0] = x / W, tm[1 + i] = V_i halo'd tiles; tmm = m, tmz = z
+                           // coefficients) instead of per-thread cp.async
   CUtensorMap tm[HELM_KMAX + 1];
+  CUtensorMap tmm, tmz;
+  int tmq;                 // with tma: m and the z coefficients by TMA too (else per-thread cp.async)
   KCtx ctx;
   RedBuf rb;
 };
@@ -108,7 +123,12 @@ template <typename R> struct PlaneArgs {
 template <typename R, int BX, int BY, int NX, int NP, bool YC>
 struct PlaneSmem {
   static constexpr int YH = YC ? 1 : 0;              // y-halo rows (3D only)
-  static constexpr int XE = (BY + 2 * YH) * (BX + 2); // halo tile elements
+  // TMA boxes must start 16-B aligned along x (measured on B200: an unaligned start faults
+  // with an illegal instruction, scripts/tma_probe.cu), so the tile's first interior column
+  // sits XO = 16 B / element into the row: complex128 1, complex64 2 (one unused column)
+  static constexpr int XO = (int)(16 / sizeof(cx<R>));
+  static constexpr int XP = BX + 2 * XO;              // shared row pitch (elements)
+  static constexpr int XE = (BY + 2 * YH) * XP;       // halo tile elements
   // tile stride in elements, padded to 128 B (TMA destinations must be 128-B aligned)
   static constexpr int XS = (int)(((XE * sizeof(cx<R>) + 127) / 128 * 128) / sizeof(cx<R>));
   static constexpr int PE = BY * BX;                 // own-point elements
@@ -120,8 +140,8 @@ struct PlaneSmem {
   static constexpr size_t m_off = (size_t)NX * XS * sizeof(cx<R>);
   static constexpr size_t p_off = m_off + (MR ? PE * sizeof(R) : 0);
   static constexpr size_t z_off = p_off + (size_t)NP * PE * sizeof(cx<R>);
-  static constexpr int ZR = YC ? 1 : BY;               // z-coefficient triples (2D: one per warp)
-  static constexpr size_t stage_bytes = (z_off + ZR * 3 * sizeof(cx<R>) + 127) / 128 * 128;
+  static constexpr int ZR = YC ? 1 : BY;               // z-coefficient rows (2D: one per warp)
+  static constexpr size_t stage_bytes = (z_off + ZR * 4 * sizeof(cx<R>) + 127) / 128 * 128;
 };
 
 // MODE 4 = MODE 3 for the LAST step of a cycle: Y = H V_NV is not stored, and ||Y||^2 is
@@ -228,7 +248,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
   constexpr int YH = SM::YH;
   constexpr int NT = BX * BY / PY;
   constexpr int RS = BY / PY;          // row stride between a thread's rows
-  constexpr int XP = BX + 2;           // shared row pitch (elements)
+  constexpr int XP = SM::XP, XO = SM::XO;   // shared row pitch, first interior column
   constexpr bool FORM = MODE >= 3 && NV > 0;
   constexpr bool LAST = MODE == 4;
   static_assert(YC || PY == 1, "2D (rows = RHS) uses one row per thread");
@@ -285,6 +305,10 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
     __syncthreads();
   }
   unsigned pbits = 0;      // parity of the next TMA fill of each stage
+  // per-thread cp.async groups: everything without TMA; with TMA only MODE 1/2's own points
+  const bool tmq = tma && a.tmq != 0;
+  const bool cpa_on = !tmq || MODE == 1 || MODE == 2;
+  const int zrow0 = (g.rop ? g.rop[rhs[0]] : 0) * nz;   // this RHS's rows of the z table
   double2 acc[NVR];
 #pragma unroll
   for (int k = 0; k < NVR; ++k) acc[k] = make_double2(0.0, 0.0);
@@ -328,16 +352,16 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
 #pragma unroll
     for (int k = 0; k < PY; ++k) {
       const int sr = ty0 + k * RS + YH;
-      lg[k] = gofs[k]; ls[k] = (unsigned)((sr * XP + tx + 1) * sizeof(C)); lp[k] = rok[k]; lh[k] = true;
-      lg[PY + k] = gofs[k] - 1; ls[PY + k] = (unsigned)(sr * XP * sizeof(C));
+      lg[k] = gofs[k]; ls[k] = (unsigned)((sr * XP + tx + XO) * sizeof(C)); lp[k] = rok[k]; lh[k] = true;
+      lg[PY + k] = gofs[k] - 1; ls[PY + k] = (unsigned)((sr * XP + XO - 1) * sizeof(C));
       lp[PY + k] = rok[k] && ix > 0; lh[PY + k] = tx == 0;
-      lg[2 * PY + k] = gofs[k] + 1; ls[2 * PY + k] = (unsigned)((sr * XP + BX + 1) * sizeof(C));
+      lg[2 * PY + k] = gofs[k] + 1; ls[2 * PY + k] = (unsigned)((sr * XP + BX + XO) * sizeof(C));
       lp[2 * PY + k] = rok[k] && ix + 1 < nx; lh[2 * PY + k] = tx == BX - 1;
     }
     if constexpr (YC) {
-      lg[3 * PY] = gofs[0] - nx; ls[3 * PY] = (unsigned)((tx + 1) * sizeof(C));
+      lg[3 * PY] = gofs[0] - nx; ls[3 * PY] = (unsigned)((tx + XO) * sizeof(C));
       lp[3 * PY] = ix < nx && rowv[0] - 1 >= 0 && rowv[0] - 1 < ny; lh[3 * PY] = ty0 == 0;
-      lg[3 * PY + 1] = gofs[PY - 1] + nx; ls[3 * PY + 1] = (unsigned)(((BY + 1) * XP + tx + 1) * sizeof(C));
+      lg[3 * PY + 1] = gofs[PY - 1] + nx; ls[3 * PY + 1] = (unsigned)(((BY + 1) * XP + tx + XO) * sizeof(C));
       lp[3 * PY + 1] = ix < nx && rowv[PY - 1] + 1 < ny; lh[3 * PY + 1] = ty0 + (PY - 1) * RS == BY - 1;
     }
     const long long mofs0 = YC ? (long long)rowv[0] * nx + ix : (long long)ix;
@@ -353,12 +377,18 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           if (threadIdx.x == 0) {
             fence_proxy_async();   // the stage's previous contents were read / formed by the generic proxy
             const unsigned bar = mbase + 8 * stg;
-            mbar_expect_tx(bar, (unsigned)(NX * SM::XE * sizeof(C)));   // full boxes (OOB zero-filled)
-            constexpr int CR = (int)(sizeof(C) / sizeof(R));   // tensor element = one real
+            // full boxes (OOB zero-filled): the halo'd tiles, m's own points, the z row
+            mbar_expect_tx(bar, (unsigned)(NX * SM::XE * sizeof(C) +
+                                           (tmq ? (SM::MR ? SM::PE * sizeof(R) : 0) + 4 * sizeof(C) : 0)));
+            constexpr int CR = (int)(sizeof(C) / 8);   // tensor element = one 8-byte word
 #pragma unroll
             for (int t = 0; t < NX; ++t)
-              tma_load4(st + (unsigned)(t * SM::XS * sizeof(C)), &a.tm[t], bar, CR * (txb * BX - 1), tyb * BY - YH, z,
+              tma_load4(st + (unsigned)(t * SM::XS * sizeof(C)), &a.tm[t], bar, CR * (txb * BX - XO), tyb * BY - YH, z,
                         rhs[0]);
+            if (tmq) {
+              if constexpr (SM::MR) tma_load3(st + (unsigned)SM::m_off, &a.tmm, bar, txb * BX, tyb * BY, z);
+              tma_load2(st + (unsigned)SM::z_off, &a.tmz, bar, 0, zrow0 + z);
+            }
           }
           pbits ^= 1u << stg;
         } else {
@@ -374,18 +404,19 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           }
         }
         if (q >= 1 && z < z1) {
-          if ((YC ? threadIdx.x : tx) < 3) {   // z coefficients of plane z: lo, dg, up (ghosts masked, R7)
+          if (!tmq && (YC ? threadIdx.x : tx) < 3) {   // z coefficients of plane z: lo, dg, up (ghosts masked, R7)
             const int c3 = YC ? threadIdx.x : tx;
             const C* tz = c3 == 0 ? T.lo[2] : (c3 == 1 ? T.dg[2] : T.up[2]);
             const bool p = c3 == 1 || (c3 == 0 ? z > 0 : z < nz - 1);
-            cpa<sizeof(C)>(st + (unsigned)(SM::z_off + ((YC ? 0 : ty0) * 3 + c3) * sizeof(C)), p ? tz + z : tz, p);
+            cpa<sizeof(C)>(st + (unsigned)(SM::z_off + ((YC ? 0 : ty0) * 4 + c3) * sizeof(C)), p ? tz + z : tz, p);
           }
 #pragma unroll
           for (int k = 0; k < PY; ++k)
             if (rok[k]) {
               const int pr = (ty0 + k * RS) * BX + tx;
               if constexpr (SM::MR)
-                cpa<sizeof(R)>(st + (unsigned)(SM::m_off + pr * sizeof(R)), g.m + (YC ? mofs0 + (long long)k * RS * nx : mofs0) + zo, true);
+                if (!tmq)
+                  cpa<sizeof(R)>(st + (unsigned)(SM::m_off + pr * sizeof(R)), g.m + (YC ? mofs0 + (long long)k * RS * nx : mofs0) + zo, true);
               if constexpr (MODE == 1) cpa<sizeof(C)>(st + (unsigned)(SM::p_off + pr * sizeof(C)), a.b + gofs[k] + zo, true);
               if constexpr (MODE == 2) {
 #pragma unroll
@@ -395,7 +426,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
             }
         }
       }
-      cpa_commit();   // always commit (possibly empty) so group counting stays uniform
+      if (cpa_on) cpa_commit();   // always commit (possibly empty) so group counting stays uniform
     };
     // MODE 3: turn the raw W tile of stage `q` into V_NV in place (halo included)
     auto form = [&](int stg) {
@@ -411,9 +442,9 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           for (int e = threadIdx.x; e < SM::XE; e += NT) f1(e);
         } else {
           const int rowe = ty0 * XP;
-          f1(rowe + tx + 1);
-          if (tx == 0) f1(rowe);
-          if (tx == BX - 1) f1(rowe + BX + 1);
+          f1(rowe + tx + XO);
+          if (tx == 0) f1(rowe + XO - 1);
+          if (tx == BX - 1) f1(rowe + BX + XO);
         }
       }
     };
@@ -451,7 +482,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
     if constexpr (!SM::MR) { ldm(z0, mr0); ldm(z0 + 1, mr1); }
     for (int z = z0; z < z1; ++z) {
       const int q = z - z0 + 1;
-      cpa_wait_n(S - 4);        // this thread's groups <= q+1 complete (committed: <= q+S-3)
+      if (cpa_on) cpa_wait_n(S - 4);   // this thread's groups <= q+1 complete (committed: <= q+S-3)
       if (tma) {                // ... and the TMA tiles of planes <= q+1 (stage s_m1 + 2)
         const int sw = inc(inc(s_m1));
         if (z == z0) {
@@ -477,12 +508,12 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
       if constexpr (!SM::MR) ldm(z + 2, mr2);
       const C* Ps = reinterpret_cast<const C*>(st1 + SM::p_off);
       const C* Zt = reinterpret_cast<const C*>(st1 + SM::z_off);
-      const C lz = Zt[(YC ? 0 : ty0) * 3], dz = Zt[(YC ? 0 : ty0) * 3 + 1], uz = Zt[(YC ? 0 : ty0) * 3 + 2];
+      const C lz = Zt[(YC ? 0 : ty0) * 4], dz = Zt[(YC ? 0 : ty0) * 4 + 1], uz = Zt[(YC ? 0 : ty0) * 4 + 2];
       const long long zo = (long long)z * plane;
 #pragma unroll
       for (int k = 0; k < PY; ++k) {
         if (!rok[k]) continue;
-        const int c = (ty0 + k * RS + YH) * XP + tx + 1;
+        const int c = (ty0 + k * RS + YH) * XP + tx + XO;
         const int pr = (ty0 + k * RS) * BX + tx;
         const C cur = X1[c];
         const R wm = T.w2 * (SM::MR ? Ms[pr] : mr0[k]);
