@@ -317,14 +317,19 @@ template <int N = 0, typename F> void dispatch_k0(int k, F&& f) {
 // 32 x-points x 8 right-hand sides). The ring depth S is a launch parameter: the largest
 // S <= 12 whose ring fits the shared-memory budget of `occ_target` CTAs per SM (default 4;
 // HELM_PLANE_OCC / HELM_PLANE_S override, for tuning).
-template <int MODE, bool YC> constexpr int plane_py() { return (YC && MODE < 3) ? 2 : 1; }
+// Rows per thread: 4 for the plain matvec (halves the per-plane fixed cost per point: measured
+// +15-35 % on the cfg5 sweep, profiles/r01/matvec_py_ab.txt), 2 for MODE 1/2, 1 for the
+// register-heavy Arnoldi steps.
+template <int MODE, bool YC> constexpr int plane_py() { return !YC ? 1 : (MODE == 0 ? 4 : (MODE < 3 ? 2 : 1)); }
 
 // Ring depth S = smem budget / (occupancy target x stage bytes). Measured on the cfg5 matvec
 // (profiles/r01/matvec_occ_ab.txt): complex64 stages are half the bytes, and its kernels are
 // issue-latency bound, so it wants more resident CTAs (8) over a deeper ring; complex128 4.
+// The 64-thread matvec CTAs (PY = 4) want 12 (complex64) / 6 (complex128).
 struct PlaneTune { int occ_target, s_fixed; };
-template <typename R> const PlaneTune& plane_tune() {
-  static const PlaneTune t{std::max(1, env_int("HELM_PLANE_OCC", sizeof(R) == 4 ? 8 : 4)), env_int("HELM_PLANE_S", 0)};
+template <typename R, int PY> const PlaneTune& plane_tune() {
+  static const PlaneTune t{std::max(1, env_int("HELM_PLANE_OCC", PY == 4 ? (sizeof(R) == 4 ? 12 : 6) : (sizeof(R) == 4 ? 8 : 4))),
+                           env_int("HELM_PLANE_S", 0)};
   return t;
 }
 
@@ -420,16 +425,19 @@ PlaneSplit plane_split(int groups, long long G, int T, int nz) {
 }
 
 // Launch with exactly one resident wave (groups x cpg CTAs, see stencil.cuh).
-template <typename R, int MODE, int NV, bool YC>
+template <typename R, int MODE, int NV, bool YC, int PY = plane_py<MODE, YC>()>
 void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
-  constexpr int PY = plane_py<MODE, YC>();
+  if constexpr (MODE == 0 && PY == 4) {   // HELM_PLANE_PY=2: two rows per thread (A/B)
+    static const bool py2 = env_int("HELM_PLANE_PY", 4) == 2;
+    if (py2) { run_plane<R, MODE, NV, YC, 2>(a, groups, units, st); return; }
+  }
   using Sh = PlaneShape<MODE, NV>;
   constexpr int NT = 32 * 8 / PY;
   constexpr size_t sb = PlaneSmem<R, 32, 8, Sh::NX, Sh::NP, YC>::stage_bytes;
   auto kern = k_plane<R, 32, 8, PY, MODE, NV, YC>;
   static const PlaneCfg cfg = [&] {
     PlaneCfg c;
-    const PlaneTune& t = plane_tune<R>();
+    const PlaneTune& t = plane_tune<R, PY>();
     c.S = t.s_fixed >= 4 ? std::min(t.s_fixed, 12) : (int)std::min<size_t>(12, (220 * 1024) / (t.occ_target * sb));
     c.S = std::max(c.S, 4);
     c.smem = c.S * sb + 8 * c.S;   // ring + one mbarrier per stage (TMA)

@@ -403,7 +403,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
               }
           }
         }
-        if (q >= 1 && z < z1) {
+        if (cpa_on && q >= 1 && z < z1) {   // per-thread operands (none for MODE 0/3/4 with TMA)
           if (!tmq && (YC ? threadIdx.x : tx) < 3) {   // z coefficients of plane z: lo, dg, up (ghosts masked, R7)
             const int c3 = YC ? threadIdx.x : tx;
             const C* tz = c3 == 0 ? T.lo[2] : (c3 == 1 ? T.dg[2] : T.up[2]);
