@@ -320,7 +320,10 @@ template <int N = 0, typename F> void dispatch_k0(int k, F&& f) {
 // Rows per thread: 4 for the plain matvec (halves the per-plane fixed cost per point: measured
 // +15-35 % on the cfg5 sweep, profiles/r01/matvec_py_ab.txt), 2 for MODE 1/2, 1 for the
 // register-heavy Arnoldi steps.
-template <int MODE, bool YC> constexpr int plane_py() { return !YC ? 1 : (MODE == 0 ? 4 : (MODE < 3 ? 2 : 1)); }
+#ifndef HELM_PY34
+#define HELM_PY34 2   // Arnoldi steps: 2 rows per thread (3D solve A/B: c128 -2..4 %, c64 -15 %)
+#endif
+template <int MODE, bool YC> constexpr int plane_py() { return !YC ? 1 : (MODE == 0 ? 4 : (MODE < 3 ? 2 : HELM_PY34)); }
 
 // Ring depth S = smem budget / (occupancy target x stage bytes). Measured on the cfg5 matvec
 // (profiles/r01/matvec_occ_ab.txt): complex64 stages are half the bytes, and its kernels are
