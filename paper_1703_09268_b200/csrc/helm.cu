@@ -507,8 +507,13 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
     const long long cost = ((items + wpr - 1) / wpr) * (zl + 2 + S / 2);
     if (best < 0 || cost < best) { best = cost; nzc_b = nzc; zl_b = zl; }
   }
+  static const int nzc_fix = env_int("HELM_MARCH_NZC", 0);   // tuning: force the z-chunk count
+  if (nzc_fix > 0) { zl_b = (nz + nzc_fix - 1) / nzc_fix; nzc_b = (nz + zl_b - 1) / zl_b; }
   a.nzc = nzc_b; a.zlen = zl_b;
   a.wpr = (int)std::min<long long>(wpr, (long long)a.nstrip * nzc_b);
+  if (env_int("HELM_DEBUG", 0) > 1)
+    std::fprintf(stderr, "[helm] march2d nx=%d nz=%d nrhs=%d W=%lld wpr=%d nstrip=%d nzc=%d zlen=%d S=%d\n", a.g.nx, nz,
+                 a.nrhs, W, a.wpr, a.nstrip, a.nzc, a.zlen, S);
   const long long warps = (long long)a.nrhs * a.wpr;
   pdl_launch(kern, dim3((unsigned)((warps + 3) / 4)), dim3(128), smem, st, a);
 }
