@@ -500,11 +500,16 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
   const int nz = a.g.nz;
   long long best = -1;
   int nzc_b = 1, zl_b = nz;
-  for (int n = 1; n <= nz; ++n) {   // z-chunk count minimising rounds x (chunk + halo + ring fill)
+  // z-chunk count minimising rounds x (chunk + halo + ring fill) + the slot reduction of the
+  // last-arriving warp (one L2 round trip per 128 warps of the RHS, worth ~red_w plane steps):
+  // small late-cycle batches otherwise spread one RHS over thousands of 1-plane items
+  static const int red_w = env_int("HELM_MARCH_RED", 8);   // bench A/B: 8 vs 0 = +3 %
+  for (int n = 1; n <= nz; ++n) {
     const int zl = (nz + n - 1) / n, nzc = (nz + zl - 1) / zl;
     if (nzc != n) continue;
     const long long items = (long long)a.nstrip * nzc;
-    const long long cost = ((items + wpr - 1) / wpr) * (zl + 2 + S / 2);
+    const long long used = std::min<long long>(wpr, items);
+    const long long cost = ((items + wpr - 1) / wpr) * (zl + 2 + S / 2) + red_w * ((used + 127) / 128);
     if (best < 0 || cost < best) { best = cost; nzc_b = nzc; zl_b = zl; }
   }
   static const int nzc_fix = env_int("HELM_MARCH_NZC", 0);   // tuning: force the z-chunk count

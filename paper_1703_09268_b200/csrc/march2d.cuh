@@ -203,8 +203,15 @@ k_march2d(const MarchArgs<R> a) {
   // z coefficients of every operator of the level (packed, ghosts masked, R7) in shared
   // memory: one contiguous copy per CTA
   extern __shared__ __align__(16) unsigned char msm[];
+  // (cp.async: every element in flight at once — a load/store loop here cost several L2
+  // round trips per launch, a fixed latency that dominated the small late-cycle batches)
   C* zt = reinterpret_cast<C*>(msm);
-  for (int e = threadIdx.x; e < 3 * g.nop * nz; e += blockDim.x) zt[e] = g.zpk[e];
+  {
+    const unsigned zs = (unsigned)__cvta_generic_to_shared(zt);
+    for (int e = threadIdx.x; e < 3 * g.nop * nz; e += blockDim.x) cpa<sizeof(C)>(zs + e * (unsigned)sizeof(C), g.zpk + e, true);
+    cpa_commit();
+    cpa_wait<0>();
+  }
   __syncthreads();
   if (ia >= a.nrhs) return;
   if (a.kact && a.jskip >= a.kact[r]) return;

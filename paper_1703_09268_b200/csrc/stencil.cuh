@@ -182,7 +182,25 @@ __device__ __forceinline__ bool warp_slot_reduce(double2 (&v)[NV], double2* part
   __threadfence();
 #pragma unroll
   for (int k = 0; k < NV; ++k) tot[k] = make_double2(0.0, 0.0);
-  for (int sl = lane; sl < nslots; sl += 32) {
+  // four slots per lane per round, all loads issued before the adds (the sum over a lane's
+  // slots was a chain of dependent L2 round trips: several us per launch at small batches);
+  // the summation order is fixed by the slot index, so results stay bitwise reproducible
+  int sl = lane;
+  for (; sl + 96 < nslots; sl += 128) {
+    double2 t[4][NV];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) t[u][k] = __ldcg(part + (size_t)(sl + 32 * u) * NV + k);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        tot[k].x += t[u][k].x;
+        tot[k].y += t[u][k].y;
+      }
+  }
+  for (; sl < nslots; sl += 32) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const double2 t = __ldcg(part + (size_t)sl * NV + k);
