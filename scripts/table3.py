@@ -1,0 +1,73 @@
+"""the paper's Table 3 preconditioner study as a workload.
+3D constant velocity, n_lambda wavelengths per axis at n_ppw points per wavelength, PML of one
+wavelength per side, centred point source, ML-GMRES (3,5,3,5) inside FGMRES(5), rel. residual
+1e-6, complex128, one RHS per solve. For each cell: our outer FGMRES cycles (7-pt STD2 stencil;
+the paper's counts used a 27-pt stencil, so they are context, not a parity target, R4), the
+certified true residual, the device time of the solve (CUDA events, after one untimed solve),
+and the paper's count and CPU time (Table 3). One JSON line per cell.
+
+    python scripts/table3.py [--cells 5x6,10x8,...] [--reps 1]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_1703_09268_b200 import api  # noqa: E402
+
+GOLD = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                                   "paper_values.json")))
+PAPER_TIME = {  # Table 3: overall computational time in seconds (CPU, 5 threads per matvec)
+    (5, 6): 4.6, (5, 8): 6.9, (5, 10): 10.8, (10, 6): 28.9, (10, 8): 38.8, (10, 10): 76.8,
+    (25, 6): 809, (25, 8): 615, (25, 10): 1009.8, (40, 6): 4545, (40, 8): 2795, (40, 10): 4747,
+    (50, 6): 11789, (50, 8): 5741, (50, 10): 10373}
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cells", default="")
+ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--dtype", default="c128")
+ap.add_argument("--max-outer", type=int, default=50)
+a = ap.parse_args()
+cells = [tuple(int(v) for v in c.split("x")) for c in a.cells.split(",") if c] or synth.TABLE3_CELLS
+dt = api.C64 if a.dtype == "c64" else api.C128
+td = torch.complex64 if dt == api.C64 else torch.complex128
+for nl, npw in cells:
+    p = synth.table3(nl, npw)
+    w = 2 * np.pi * p.freqs[0]
+    t0 = time.perf_counter()
+    op = api.helm_setup(api.Grid.of(p), p.m, w, api.Pml(v_ref=2000.0), dt, max_rhs=1)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    nx, ny, nz = p.next
+    b = torch.zeros(1, p.n_ext, dtype=td, device="cuda")
+    s = int(p.src[0])
+    ix, iy, iz = s % p.n[0], (s // p.n[0]) % p.n[1], s // (p.n[0] * p.n[1])
+    b[0, ((iz + npw) * ny + iy + npw) * nx + ix + npw] = 1.0 / p.h**3
+    x = torch.empty_like(b)
+    so = api.SolveOpts(rtol=1e-6, max_outer=a.max_outer)
+    rep = api.helm_solve(op, b, x, opts=so)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.reps):
+        rep = api.helm_solve(op, b, x, opts=so)
+    e1.record()
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3 / a.reps
+    r = rep[0]
+    paper_it = GOLD["table3_outer_iterations"]["value"][str(nl)][(6, 8, 10).index(npw)]
+    print(json.dumps({"n_lambda": nl, "n_ppw": npw, "grid": p.next[0], "paper_grid":
+                      GOLD["table3_grid_points_per_axis"]["value"][str(nl)][(6, 8, 10).index(npw)],
+                      "points": p.n_ext, "dtype": a.dtype, "outer_cycles": r["outer_cycles"],
+                      "paper_outer_iterations": paper_it, "converged": r["converged"],
+                      "rel_residual": r["rel_residual"], "solve_s": round(sec, 3), "setup_s": round(t_setup, 2),
+                      "paper_s": PAPER_TIME[(nl, npw)], "speedup_vs_paper": round(PAPER_TIME[(nl, npw)] / sec, 1),
+                      "GBps_alg": round(r["bytes_alg"] / sec / 1e9, 1)}), flush=True)
+    del op, b, x
+    torch.cuda.empty_cache()

@@ -8,5 +8,5 @@ other. Recipes follow SURVEY.md §8(d) d.1 and are restated in DESIGN.md §3.
 """
 from .configs import (  # noqa: F401
     Problem, cfg1, cfg2, cfg3, cfg3_batch, cfg4, cfg4_replica, cfg5, tiny2d, tiny3d,
-    const_problem, random_complex, random_real, node_id, table3_grid,
+    const_problem, random_complex, random_real, node_id, table3_grid, table3, TABLE3_CELLS,
 )

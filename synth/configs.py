@@ -183,6 +183,19 @@ def table3_grid(n_lambda: int, n_ppw: int) -> int:
     return n_lambda * n_ppw + 2 * n_ppw + 1
 
 
+TABLE3_CELLS = [(nl, npw) for nl in (5, 10, 25, 40, 50) for npw in (6, 8, 10)]
+
+
+def table3(n_lambda: int, n_ppw: int, v: float = 2000.0, f: float = 10.0) -> Problem:
+    """Table 3's study: 3D constant velocity with n_lambda wavelengths per axis
+    sampled at n_ppw points per wavelength, plus a PML of one wavelength (n_ppw points) on each
+    side, centred point source. Scale-free: h = (v / f) / n_ppw; the interior has
+    n_lambda n_ppw + 1 points per axis, the extended grid table3_grid(n_lambda, n_ppw)."""
+    n = n_lambda * n_ppw + 1
+    h = v / f / n_ppw
+    return const_problem(f"table3_{n_lambda}_{n_ppw}", 3, (n, n, n), h, n_ppw, v, f, [(n // 2, n // 2, n // 2)])
+
+
 # ----------------------------------------------------------------------------- tiny cases
 def tiny2d(nx=37, nz=29, pml=7, h=10.0, f=9.0, nsrc=3, seed=0) -> Problem:
     """Small heterogeneous 2D problem used by fast tests (ragged sizes on purpose)."""

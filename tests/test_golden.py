@@ -38,3 +38,18 @@ def test_dot_test_at_paper_magnitude():
     a, b = np.vdot(y, H @ x), np.vdot(H.conj().T @ y, x)
     rel = abs(a - b) / max(abs(a), abs(b))
     assert rel < 100 * G["table5_helmholtz_dot_test_rel_diff"]["value"]
+
+
+def test_table3_workload_generator():
+    """synth.table3 builds every Table 3 cell with the R17 grid rule, one
+    wavelength of PML (n_ppw points) per side, h = lambda / n_ppw and a centred source."""
+    for nl, ppw in synth.TABLE3_CELLS:
+        p = synth.table3(nl, ppw)
+        n = synth.table3_grid(nl, ppw)
+        assert p.next == (n, n, n)
+        assert all(w == (ppw, ppw) for w in p.pml)
+        lam = 1.0 / np.sqrt(p.m.max()) / p.freqs[0]
+        assert abs(lam / p.h - ppw) < 1e-12
+        assert abs(p.n[0] * p.h - (nl * lam + p.h)) < 1e-9 * lam   # n_lambda wavelengths (+ one node)
+        s = int(p.src[0])
+        assert (s % p.n[0], (s // p.n[0]) % p.n[1], s // (p.n[0] * p.n[1])) == (p.n[0] // 2,) * 3
