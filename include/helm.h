@@ -80,6 +80,20 @@ typedef struct {
   double bytes_alg;
 } helm_solve_report;
 
+/* Off-grid acquisition ("Kaiser-windowed sinc interpolation"; SURVEY §8(f) rank 4;
+ * DESIGN R33). Coordinates are physical (grid units of h), relative to interior node (0,0,0),
+ * host fp64 triples (x, y, z) — 2D grids need y = 0; every point must lie inside the interior
+ * box [0, (n_a - 1) h] (else HELM_ERR_ARG naming the point). Rows of P: tensor products of 1D
+ * weights sinc(t-k) I0(b sqrt(1-((t-k)/r)^2)) / I0(b), |t-k| <= r, each axis normalised to
+ * sum 1 (an on-node point is the on-node delta). kaiser_b <= 0 selects 6.31, half_width <= 0
+ * selects 4 (max 8). The source of point s is S(omega) P_s^T e_s / h^d. */
+typedef struct {
+  const double* src_xyz;   /* [nsrc_total][3] */
+  const double* rec_xyz;   /* [nrec][3] */
+  double kaiser_b;
+  int32_t half_width;
+} helm_acq;
+
 typedef struct helm_op helm_op;   /* opaque */
 
 /* a1 (Fig. 3). Builds, on the device: m_ext = E m (D2), the per
@@ -169,6 +183,24 @@ helm_status fwi_gn_hessian(const helm_grid* grid, const double* m_slowness2, int
                            const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts,
                            int32_t max_rhs, double* h_dev, helm_solve_report* report_host,
                            void* cuda_stream);
+
+/* ---- off-grid acquisition (helm_acq above): Listing 1 OBJ and FORW_MODEL with interpolated
+ * P_s, P_r. Same arguments and outputs as fwi_misfit_grad / fwi_forward with the node-id
+ * arrays replaced by `acq` (nsrc_total = number of source points, nrec = receiver points);
+ * receivers need not be distinct nodes. */
+helm_status fwi_misfit_grad_acq(const helm_grid* grid, const double* m_slowness2, int32_t nfreq,
+                                const double* freq_hz, const double* src_weight_reim,
+                                int32_t nsrc_total, int32_t src_begin, int32_t src_end,
+                                int32_t nrec, const helm_acq* acq, const double* d_obs_reim,
+                                const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts,
+                                int32_t max_rhs, double* fg_dev, helm_solve_report* report_host,
+                                void* cuda_stream);
+helm_status fwi_forward_acq(const helm_grid* grid, const double* m_slowness2, int32_t nfreq,
+                            const double* freq_hz, const double* src_weight_reim,
+                            int32_t nsrc_total, int32_t src_begin, int32_t src_end, int32_t nrec,
+                            const helm_acq* acq, const helm_pml* pml, helm_dtype dtype,
+                            const helm_solve_opts* opts, int32_t max_rhs, double* d_host,
+                            helm_solve_report* report_host, void* cuda_stream);
 
 /* ---- inspection entry points (same op; used by the parity tests) ---------------------- */
 

@@ -32,6 +32,11 @@ class HelmSolveOpts(C.Structure):
     _fields_ = [("k_inner", C.c_int32), ("max_outer", C.c_int32), ("rtol", C.c_double), ("precond", C.c_int32)]
 
 
+class HelmAcq(C.Structure):
+    _fields_ = [("src_xyz", C.POINTER(C.c_double)), ("rec_xyz", C.POINTER(C.c_double)), ("kaiser_b", C.c_double),
+                ("half_width", C.c_int32)]
+
+
 class HelmSolveReport(C.Structure):
     _fields_ = [("outer_cycles", C.c_int32), ("converged", C.c_int32), ("rel_residual", C.c_double),
                 ("matvecs", C.c_int64 * 4), ("bytes_alg", C.c_double)]
@@ -72,6 +77,12 @@ SIGNATURES = {
     "fwi_gn_hessian": (C.c_int, [C.POINTER(HelmGrid), _d, C.c_int32, _d, _d, C.c_int32, C.c_int32, _i64,
                                  C.c_int32, _i64, _d, C.POINTER(HelmPml), C.c_int, C.POINTER(HelmSolveOpts),
                                  C.c_int32, _P, _rep, _P]),
+    "fwi_misfit_grad_acq": (C.c_int, [C.POINTER(HelmGrid), _d, C.c_int32, _d, _d, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_int32, C.POINTER(HelmAcq), _d, C.POINTER(HelmPml), C.c_int,
+                                      C.POINTER(HelmSolveOpts), C.c_int32, _P, _rep, _P]),
+    "fwi_forward_acq": (C.c_int, [C.POINTER(HelmGrid), _d, C.c_int32, _d, _d, C.c_int32, C.c_int32, C.c_int32,
+                                  C.c_int32, C.POINTER(HelmAcq), C.POINTER(HelmPml), C.c_int, C.POINTER(HelmSolveOpts),
+                                  C.c_int32, _d, _rep, _P]),
     "helm_levels": (C.c_int, [_P, C.POINTER(C.c_int32), _i64]),
     "helm_get_level": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64, _d, _d]),
     "helm_vcycle": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),

@@ -65,6 +65,23 @@ class Pml:
 
 
 @dataclasses.dataclass(frozen=True)
+class Acq:
+    """Off-grid acquisition (helm.h helm_acq, DESIGN R33): physical (x, y, z) of the source and
+    receiver points relative to interior node 0 (y = 0 in 2D); Kaiser window b and half-width
+    (<= 0: 6.31 and 4)."""
+    src_xyz: np.ndarray
+    rec_xyz: np.ndarray
+    kaiser_b: float = 0.0
+    half_width: int = 0
+
+    def c(self):
+        s = np.ascontiguousarray(self.src_xyz, np.float64).reshape(-1, 3)
+        r = np.ascontiguousarray(self.rec_xyz, np.float64).reshape(-1, 3)
+        st = L.HelmAcq(_dptr(s), _dptr(r), float(self.kaiser_b), int(self.half_width))
+        return st, (s, r), len(s), len(r)
+
+
+@dataclasses.dataclass(frozen=True)
 class SolveOpts:
     k_inner: int = 5
     max_outer: int = 50
@@ -315,6 +332,49 @@ def fwi_gn_hessian(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], 
                                _i64ptr(src), len(rec), _i64ptr(rec), _dptr(dmv), C.byref(p), dtype, C.byref(so),
                                max_rhs, _tptr(out), rep, _stream(stream)))
     return out, [rep[i].as_dict() for i in range(nrep)]
+
+
+def fwi_misfit_grad_acq(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], acq: Acq, d_obs: np.ndarray,
+                        pml: Pml, dtype: int = C128, opts: SolveOpts = SolveOpts(), max_rhs: int = 16,
+                        src_range: Optional[Tuple[int, int]] = None, weights=None,
+                        fg: Optional[torch.Tensor] = None, stream=None):
+    """Listing 1 `case OBJ` with off-grid (Kaiser-sinc) sources and receivers: (fg, reports)."""
+    lib = L.load()
+    m = np.ascontiguousarray(m_slowness2, np.float64)
+    d = np.ascontiguousarray(d_obs, np.complex128)
+    f, w = _freq_args(freqs, weights)
+    ac, keep, ns_tot, nrec = acq.c()
+    s0, s1 = (0, ns_tot) if src_range is None else src_range
+    if fg is None:
+        fg = torch.empty(1 + grid.n_interior, dtype=torch.float64, device="cuda")
+    nrep = len(f) * (s1 - s0) * 2
+    rep = (L.HelmSolveReport * max(nrep, 1))()
+    g, p, so = grid.c(), pml.c(), opts.c()
+    L.check(lib.fwi_misfit_grad_acq(C.byref(g), _dptr(m), len(f), _dptr(f), None if w is None else _dptr(w), ns_tot, s0,
+                                    s1, nrec, C.byref(ac), _dp(d), C.byref(p), dtype, C.byref(so), max_rhs, _tptr(fg),
+                                    rep, _stream(stream)))
+    del keep
+    return fg, [rep[i].as_dict() for i in range(nrep)]
+
+
+def fwi_forward_acq(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], acq: Acq, pml: Pml,
+                    dtype: int = C128, opts: SolveOpts = SolveOpts(), max_rhs: int = 16,
+                    src_range: Optional[Tuple[int, int]] = None, weights=None, stream=None):
+    """Listing 1 `case FORW_MODEL` with off-grid sources and receivers: (d (nfreq, ns, nrec), reports)."""
+    lib = L.load()
+    m = np.ascontiguousarray(m_slowness2, np.float64)
+    f, w = _freq_args(freqs, weights)
+    ac, keep, ns_tot, nrec = acq.c()
+    s0, s1 = (0, ns_tot) if src_range is None else src_range
+    d = np.zeros((len(f), s1 - s0, nrec), np.complex128)
+    nrep = len(f) * (s1 - s0) * 2
+    rep = (L.HelmSolveReport * max(nrep, 1))()
+    g, p, so = grid.c(), pml.c(), opts.c()
+    L.check(lib.fwi_forward_acq(C.byref(g), _dptr(m), len(f), _dptr(f), None if w is None else _dptr(w), ns_tot, s0, s1,
+                                nrec, C.byref(ac), C.byref(p), dtype, C.byref(so), max_rhs, _dp(d), rep,
+                                _stream(stream)))
+    del keep
+    return d, [rep[i].as_dict() for i in range(0, nrep, 2)]
 
 
 # ---------------------------------------------------------------------------- measurement

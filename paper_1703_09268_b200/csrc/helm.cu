@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <tuple>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1282,6 +1283,85 @@ std::vector<long long> to_ext(const helm_grid& G, const int64_t* ids, int n) {
   return e;
 }
 
+// Off-grid points (helm_acq): Kaiser-windowed sinc rows of P (DESIGN R33) built on
+// the host — 1D weights sinc(t-k) I0(b sqrt(1-((t-k)/r)^2)) / I0(b), |t-k| <= r, normalised per
+// axis after dropping taps outside the extended grid, tensor product over the axes.
+struct TapRows {
+  std::vector<int> off{0};
+  std::vector<long long> node;
+  std::vector<double> w;
+};
+static double sinc_pi(double x) { return x == 0.0 ? 1.0 : std::sin(M_PI * x) / (M_PI * x); }
+static void ks_axis(double t, int n_ext, int lo, double b, int r, std::vector<long long>& e, std::vector<double>& w) {
+  e.clear(); w.clear();
+  double sum = 0.0;
+  const double i0b = std::cyl_bessel_i(0.0, b);
+  for (long long k = (long long)std::ceil(t - r); k <= (long long)std::floor(t + r); ++k) {
+    const long long ek = k + lo;
+    if (ek < 0 || ek >= n_ext) continue;
+    const double d = t - (double)k, q = 1.0 - (d / r) * (d / r);
+    const double wk = sinc_pi(d) * std::cyl_bessel_i(0.0, b * std::sqrt(std::max(q, 0.0))) / i0b;
+    e.push_back(ek); w.push_back(wk); sum += wk;
+  }
+  for (double& x : w) x /= sum;
+}
+static TapRows build_taps(const helm_grid& G, const double* xyz, int npts, double b, int r) {
+  TapRows T;
+  const int Ne[3] = {(int)(G.n[0] + G.pml[0][0] + G.pml[0][1]), (int)(G.n[1] + G.pml[1][0] + G.pml[1][1]),
+                     (int)(G.n[2] + G.pml[2][0] + G.pml[2][1])};
+  std::vector<long long> e[3];
+  std::vector<double> w[3];
+  for (int p = 0; p < npts; ++p) {
+    for (int a = 0; a < 3; ++a) {
+      const double c = xyz[3 * p + a];
+      if (a == 1 && G.ndim == 2) {
+        REQ(c == 0.0, HELM_ERR_ARG, "2D acquisition points need y = 0");
+        e[1].assign(1, 0); w[1].assign(1, 1.0);
+        continue;
+      }
+      REQ(std::isfinite(c) && c >= 0.0 && c <= (double)(G.n[a] - 1) * G.h, HELM_ERR_ARG,
+          "acquisition point " + std::to_string(p) + " outside the interior along axis " + std::to_string(a));
+      ks_axis(c / G.h, Ne[a], (int)G.pml[a][0], b, r, e[a], w[a]);
+    }
+    for (size_t kz = 0; kz < e[2].size(); ++kz)
+      for (size_t ky = 0; ky < e[1].size(); ++ky)
+        for (size_t kx = 0; kx < e[0].size(); ++kx) {
+          T.node.push_back((e[2][kz] * Ne[1] + e[1][ky]) * Ne[0] + e[0][kx]);
+          T.w.push_back(w[2][kz] * w[1][ky] * w[0][kx]);
+        }
+    T.off.push_back((int)T.node.size());
+  }
+  return T;
+}
+// Rows of P^T: touched nodes in increasing order, each with its (point, weight) taps in
+// increasing point order — the adjoint source is then a deterministic gather.
+struct TapRowsT {
+  std::vector<int> off{0}, pt;
+  std::vector<long long> node;
+  std::vector<double> w;
+};
+static TapRowsT transpose_taps(const TapRows& T) {
+  std::vector<std::tuple<long long, int, double>> e;
+  for (int p = 0; p + 1 < (int)T.off.size(); ++p)
+    for (int t = T.off[p]; t < T.off[p + 1]; ++t) e.emplace_back(T.node[t], p, T.w[t]);
+  std::sort(e.begin(), e.end());
+  TapRowsT R;
+  for (size_t i = 0; i < e.size(); ++i) {
+    if (i > 0 && std::get<0>(e[i]) != std::get<0>(e[i - 1])) R.off.push_back((int)i);
+    if (i == 0 || std::get<0>(e[i]) != std::get<0>(e[i - 1])) R.node.push_back(std::get<0>(e[i]));
+    R.pt.push_back(std::get<1>(e[i]));
+    R.w.push_back(std::get<2>(e[i]));
+  }
+  R.off.push_back((int)e.size());
+  if (e.empty()) R.off.assign(1, 0);
+  return R;
+}
+template <typename T> T* upload(std::vector<void*>& keep, const std::vector<T>& v, cudaStream_t st) {
+  T* d = dalloc<T>(keep, std::max<size_t>(v.size(), 1));
+  if (!v.empty()) CK(cudaMemcpyAsync(d, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+  return d;
+}
+
 // Listing 1's PDEfunc modes over this rank's (frequency, source) pairs:
 //   OBJ     f = sum 1/2 |P_r u - d|^2 and g = T^* V (2 solves per pair)
 //   FORW    d = P_r u (1 solve)
@@ -1300,7 +1380,7 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
              const double* dobs /* OBJ: d_obs, JACADJ: y; host [nfreq][nsrc_total][nrec] */,
              const double* dm /* JAC, GN: host interior */, const helm_solve_opts& so, double* out /* OBJ: [f|g],
              JACADJ/GN: g */, helm_solve_report* rep, double* d_out /* FORW, JAC: host [nfreq][ns][nrec] */,
-             cudaStream_t st) {
+             cudaStream_t st, const helm_acq* acq = nullptr /* off-grid points instead of src / rec nodes */) {
   using C = cx<R>;
   FwiBufs fb;
   const long long N = op->lev[0].N;
@@ -1336,14 +1416,49 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
   double2* amp_d = dalloc<double2>(fb.keep, B);
   double* w2_d = dalloc<double>(fb.keep, B);
   long long* srcb_d = dalloc<long long>(fb.keep, B);
-  std::vector<long long> sext = to_ext(G, src + s_begin, ns), rext = to_ext(G, rec, nrec);
-  {
+  const bool offg = acq != nullptr;
+  std::vector<long long> sext, rext;
+  // off-grid: P_s rows of this shard's sources, P_r rows and P_r^T rows on the device
+  int *ps_off = nullptr, *pr_off = nullptr, *prt_off = nullptr, *prt_pt = nullptr, nprt = 0;
+  long long *ps_node = nullptr, *pr_node = nullptr, *prt_node = nullptr;
+  double *ps_w = nullptr, *pr_w = nullptr, *prt_w = nullptr;
+  double2* rres = nullptr;
+  if (offg) {
+    const double kb = acq->kaiser_b > 0 ? acq->kaiser_b : 6.31;
+    const int kr = acq->half_width > 0 ? acq->half_width : 4;
+    REQ(kr <= 8, HELM_ERR_ARG, "half_width must be <= 8");
+    const TapRows Ps = build_taps(G, acq->src_xyz + 3 * (size_t)s_begin, ns, kb, kr);
+    const TapRows Pr = build_taps(G, acq->rec_xyz, nrec, kb, kr);
+    const TapRowsT PrT = transpose_taps(Pr);
+    ps_off = upload(fb.keep, Ps.off, st); ps_node = upload(fb.keep, Ps.node, st); ps_w = upload(fb.keep, Ps.w, st);
+    pr_off = upload(fb.keep, Pr.off, st); pr_node = upload(fb.keep, Pr.node, st); pr_w = upload(fb.keep, Pr.w, st);
+    prt_off = upload(fb.keep, PrT.off, st); prt_node = upload(fb.keep, PrT.node, st);
+    prt_pt = upload(fb.keep, PrT.pt, st); prt_w = upload(fb.keep, PrT.w, st);
+    nprt = (int)PrT.node.size();
+    rres = dalloc<double2>(fb.keep, (size_t)B * std::max(nrec, 1));
+    CK(cudaStreamSynchronize(st));   // the host tap vectors go out of scope
+  } else {
+    sext = to_ext(G, src + s_begin, ns);
+    rext = to_ext(G, rec, nrec);
     std::vector<long long> sr = rext;
     std::sort(sr.begin(), sr.end());
     REQ(std::adjacent_find(sr.begin(), sr.end()) == sr.end(), HELM_ERR_ARG, "receivers must be distinct nodes");
   }
   fb.rec_ext = dalloc<long long>(fb.keep, std::max(nrec, 1));
-  if (nrec) CK(cudaMemcpyAsync(fb.rec_ext, rext.data(), sizeof(long long) * nrec, cudaMemcpyHostToDevice, st));
+  if (nrec && !offg) CK(cudaMemcpyAsync(fb.rec_ext, rext.data(), sizeof(long long) * nrec, cudaMemcpyHostToDevice, st));
+  const unsigned gq = (unsigned)((B * (long long)std::max(nrec, 1) + 255) / 256);
+  auto rec_gather = [&](int nb, const void* Uf, const double2* d, double2* o) {   // o = P_r u - d
+    prof_count(KC_FWI);
+    k_rec_gather<R><<<gq, 256, 0, st>>>(nb, nrec, N, pr_off, pr_node, pr_w, (const C*)Uf, d, o);
+    CKL();
+  };
+  auto rec_scatterT = [&](int nb, const double2* r) {   // A = -P_r^T r
+    if (!nprt) return;
+    prof_count(KC_FWI);
+    k_rec_scatterT<R><<<(unsigned)((nb * (long long)nprt + 255) / 256), 256, 0, st>>>(nb, nprt, nrec, N, prt_off,
+                                                                                   prt_node, prt_pt, prt_w, r, (C*)fb.A);
+    CKL();
+  };
   const double hd = std::pow(G.h, (double)G.ndim);
   std::vector<helm_solve_report> rtmp(B);
   std::vector<double2> amp_h(B), dbat((size_t)B * std::max(nrec, 1));
@@ -1357,10 +1472,14 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
   };
   auto gather_out = [&](int nb, const void* Ufield) {   // d_out[f][s][:] = P_r field
     if (!nrec) return;
-    prof_count(KC_FWI);
-    k_gather_data<R><<<(unsigned)((nb * (long long)nrec + 255) / 256), 256, 0, st>>>(nb, nrec, N, fb.rec_ext,
-                                                                                (const C*)Ufield, fb.d);
-    CKL();
+    if (offg) {
+      rec_gather(nb, Ufield, nullptr, fb.d);
+    } else {
+      prof_count(KC_FWI);
+      k_gather_data<R><<<(unsigned)((nb * (long long)nrec + 255) / 256), 256, 0, st>>>(nb, nrec, N, fb.rec_ext,
+                                                                                  (const C*)Ufield, fb.d);
+      CKL();
+    }
     CK(cudaMemcpyAsync(dbat.data(), fb.d, sizeof(double2) * nb * nrec, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     for (int b = 0; b < nb; ++b)
@@ -1378,7 +1497,7 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
       const double2 S = sw ? make_double2(sw[2 * fi], sw[2 * fi + 1]) : make_double2(1.0, 0.0);
       amp_h[b] = make_double2(S.x / hd, S.y / hd);
       w2_h[b] = wop.back() * wop.back();
-      srcb_h[b] = sext[si];
+      srcb_h[b] = offg ? si : sext[si];
     }
     REQ((int)wop.size() <= HELM_MAXOP, HELM_ERR_ARG, "more than HELM_MAXOP frequencies in one batch");
     op_set_omegas(op, wop.data(), (int)wop.size());
@@ -1389,7 +1508,10 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
     // a7: inject q = S(omega) e_s / h^d
     CK(cudaMemsetAsync(fb.Bq, 0, sizeof(C) * N * nb, st));
     prof_count(KC_FWI);
-    k_inject<R><<<(nb + 127) / 128, 128, 0, st>>>(nb, N, srcb_d, amp_d, (C*)fb.Bq);
+    if (offg)   // q = S(omega) P_s^T e_s / h^d
+      k_inject_taps<R><<<nb, 256, 0, st>>>(nb, N, srcb_d, ps_off, ps_node, ps_w, amp_d, (C*)fb.Bq);
+    else
+      k_inject<R><<<(nb + 127) / 128, 128, 0, st>>>(nb, N, srcb_d, amp_d, (C*)fb.Bq);
     CKL();
     // forward solves u = H^-1 q
     solve_any(op, 0, nb, fb.Bq, fb.U, so, rtmp.data());
@@ -1411,7 +1533,20 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
       CK(cudaMemcpyAsync(fb.d, dbat.data(), sizeof(double2) * nb * nrec, cudaMemcpyHostToDevice, st));
     }
     CK(cudaMemsetAsync(fb.A, 0, sizeof(C) * N * nb, st));
-    if (nrec) {
+    if (nrec && offg) {
+      if (mode == FW_JACADJ) {
+        rec_scatterT(nb, fb.d);                                  // -P_r^T y
+      } else if (mode == FW_GN) {
+        rec_gather(nb, dU, nullptr, rres);                       // P_r Du
+        rec_scatterT(nb, rres);
+      } else {
+        rec_gather(nb, fb.U, fb.d, rres);                        // r = P_r u - d
+        prof_count(KC_FWI);
+        k_half_sumsq<<<1, 1024, 0, st>>>((long long)nb * nrec, rres, fb.f);
+        CKL();
+        rec_scatterT(nb, rres);
+      }
+    } else if (nrec) {
       if (mode == FW_JACADJ) {
         prof_count(KC_FWI);
         k_scatter_neg<R><<<(unsigned)((nb * (long long)nrec + 255) / 256), 256, 0, st>>>(nb, nrec, N, fb.rec_ext, fb.d,
@@ -1589,15 +1724,17 @@ static helm_status fwi_common(FwiMode mode, const helm_grid* grid, const double*
                               const double* freq, const double* sw, int32_t nsrc_total, int32_t s_begin, int32_t s_end,
                               const int64_t* src, int32_t nrec, const int64_t* rec, const double* dobs,
                               const double* dm, const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts,
-                              int32_t max_rhs, double* out, helm_solve_report* rep, double* d_out, void* stream) {
+                              int32_t max_rhs, double* out, helm_solve_report* rep, double* d_out, void* stream,
+                              const helm_acq* acq = nullptr) {
   return wrap([&] {
     validate_grid(grid);
-    REQ(m && freq && src && pml, HELM_ERR_ARG, "NULL argument");
+    REQ(m && freq && pml && (src || acq), HELM_ERR_ARG, "NULL argument");
+    if (acq) REQ(acq->src_xyz && (acq->rec_xyz || nrec == 0), HELM_ERR_ARG, "acq points NULL");
     REQ(nfreq >= 1, HELM_ERR_ARG, "nfreq must be >= 1");
     for (int i = 0; i < nfreq; ++i) REQ(freq[i] > 0, HELM_ERR_ARG, "frequencies must be > 0");
     REQ(pml->v_ref > 0, HELM_ERR_ARG, "fwi requires pml.v_ref > 0 (fixed PML, R31)");
     REQ(0 <= s_begin && s_begin <= s_end && s_end <= nsrc_total, HELM_ERR_ARG, "bad source range");
-    REQ(nrec >= 0 && (nrec == 0 || rec), HELM_ERR_ARG, "bad receivers");
+    REQ(nrec >= 0 && (nrec == 0 || rec || acq), HELM_ERR_ARG, "bad receivers");
     REQ(max_rhs >= 1, HELM_ERR_ARG, "max_rhs must be >= 1");
     if (mode == FW_OBJ || mode == FW_JACADJ) REQ(out && (dobs || nrec == 0), HELM_ERR_ARG, "output / data NULL");
     if (mode == FW_GN) REQ(out && dm, HELM_ERR_ARG, "output / dm NULL");
@@ -1616,10 +1753,10 @@ static helm_status fwi_common(FwiMode mode, const helm_grid* grid, const double*
     }
     if (dtype == HELM_C128)
       fwi_run<double>(op, *grid, mode, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, dm, so, out,
-                      rep, d_out, st);
+                      rep, d_out, st, acq);
     else
       fwi_run<float>(op, *grid, mode, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, dm, so, out,
-                     rep, d_out, st);
+                     rep, d_out, st, acq);
   });
 }
 
@@ -1639,6 +1776,25 @@ helm_status fwi_forward(const helm_grid* grid, const double* m, int32_t nfreq, c
   if (!d_host) { g_err = "d_host is NULL"; return HELM_ERR_ARG; }
   return fwi_common(FW_FORW, grid, m, nfreq, freq, sw, s_end, s_begin, s_end, src, nrec, rec, nullptr, nullptr, pml,
                     dtype, opts, max_rhs, nullptr, rep, d_host, stream);
+}
+
+helm_status fwi_misfit_grad_acq(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq,
+                                const double* sw, int32_t nsrc_total, int32_t s_begin, int32_t s_end, int32_t nrec,
+                                const helm_acq* acq, const double* dobs, const helm_pml* pml, helm_dtype dtype,
+                                const helm_solve_opts* opts, int32_t max_rhs, double* fg, helm_solve_report* rep,
+                                void* stream) {
+  if (!acq) { g_err = "acq is NULL"; return HELM_ERR_ARG; }
+  return fwi_common(FW_OBJ, grid, m, nfreq, freq, sw, nsrc_total, s_begin, s_end, nullptr, nrec, nullptr, dobs, nullptr,
+                    pml, dtype, opts, max_rhs, fg, rep, nullptr, stream, acq);
+}
+
+helm_status fwi_forward_acq(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq, const double* sw,
+                            int32_t nsrc_total, int32_t s_begin, int32_t s_end, int32_t nrec, const helm_acq* acq,
+                            const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts, int32_t max_rhs,
+                            double* d_host, helm_solve_report* rep, void* stream) {
+  if (!acq || !d_host) { g_err = "acq / d_host is NULL"; return HELM_ERR_ARG; }
+  return fwi_common(FW_FORW, grid, m, nfreq, freq, sw, nsrc_total, s_begin, s_end, nullptr, nrec, nullptr, nullptr,
+                    nullptr, pml, dtype, opts, max_rhs, nullptr, rep, d_host, stream, acq);
 }
 
 helm_status fwi_jacobian(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq, const double* sw,

@@ -555,3 +555,73 @@ k_solupdate_t(long long N, VPtrs<R> Z, const double* __restrict__ zscale, cx<R>*
     xr[p] = x0;
   }
 }
+
+// ---------------------------------------------------------------------------------------
+// Off-grid sources and receivers (Kaiser-windowed sinc, DESIGN R33; SURVEY
+// §8(f) rank 4). P is a sparse row set built on the host: point p has taps [off[p], off[p+1])
+// with extended-grid nodes node[t] and weights w[t] (tensor products of normalised 1D
+// windowed-sinc weights). All sums run in a fixed order (bitwise reproducible, R30).
+
+// q_b = amp_b P_s^T e_{src(b)} (B zeroed; the taps of one source are distinct nodes).
+template <typename R>
+__global__ void k_inject_taps(int nb, long long N, const long long* __restrict__ srcb, const int* __restrict__ off,
+                              const long long* __restrict__ node, const double* __restrict__ w,
+                              const double2* __restrict__ amp, cx<R>* __restrict__ B) {
+  const int b = blockIdx.x;
+  if (b >= nb) return;
+  const int s = (int)srcb[b];
+  const double2 a = amp[b];
+  for (int t = off[s] + threadIdx.x; t < off[s + 1]; t += blockDim.x)
+    B[(long long)b * N + node[t]] = from_d<cx<R>>(make_double2(a.x * w[t], a.y * w[t]));
+}
+
+// out[b][k] = (P_r u_b)_k - d[b][k]   (d may be null)
+template <typename R>
+__global__ void k_rec_gather(int nb, int nrec, long long N, const int* __restrict__ off, const long long* __restrict__ node,
+                             const double* __restrict__ w, const cx<R>* __restrict__ U, const double2* __restrict__ d,
+                             double2* __restrict__ out) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)nb * nrec) return;
+  const int b = (int)(q / nrec), k = (int)(q % nrec);
+  const cx<R>* u = U + (long long)b * N;
+  double sx = 0.0, sy = 0.0;
+  for (int t = off[k]; t < off[k + 1]; ++t) {
+    const double2 v = to_d(u[node[t]]);
+    sx += w[t] * v.x;
+    sy += w[t] * v.y;
+  }
+  if (d) { sx -= d[q].x; sy -= d[q].y; }
+  out[q] = make_double2(sx, sy);
+}
+
+// *f += 1/2 sum |r_i|^2 over n entries: one 1024-thread block, fixed order.
+__global__ void __launch_bounds__(1024) k_half_sumsq(long long n, const double2* __restrict__ r, double* f) {
+  __shared__ double sm[1024];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += 1024) s += r[i].x * r[i].x + r[i].y * r[i].y;
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = 512; h > 0; h >>= 1) {
+    if (threadIdx.x < h) sm[threadIdx.x] += sm[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *f += 0.5 * sm[0];
+}
+
+// A_b = -P_r^T r_b as a gather over the touched nodes (rows of P_r^T: node[p], taps
+// [off[p], off[p+1]) with receiver rec[t] and weight w[t]); A zeroed elsewhere.
+template <typename R>
+__global__ void k_rec_scatterT(int nb, int nnode, int nrec, long long N, const int* __restrict__ off,
+                               const long long* __restrict__ node, const int* __restrict__ rec,
+                               const double* __restrict__ w, const double2* __restrict__ r, cx<R>* __restrict__ A) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (long long)nb * nnode) return;
+  const int b = (int)(q / nnode), p = (int)(q % nnode);
+  double sx = 0.0, sy = 0.0;
+  for (int t = off[p]; t < off[p + 1]; ++t) {
+    const double2 v = r[(long long)b * nrec + rec[t]];
+    sx += w[t] * v.x;
+    sy += w[t] * v.y;
+  }
+  A[(long long)b * N + node[p]] = from_d<cx<R>>(make_double2(-sx, -sy));
+}
