@@ -460,14 +460,14 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
 // 2D: register z-march kernel (march2d.cuh), one warp per (RHS, 30-point strip, z-chunk)
 // item; exactly one resident wave of warps, split evenly over the active right-hand sides.
 // The per-lane cp.async ring holds S planes (S-2 in flight): S is the largest depth <= 16
-// whose rings fit a shared-memory budget of ~220 KB / occ_target CTAs (4 by default, i.e.
-// 16 warps per SM; HELM_MARCH_OCC / HELM_MARCH_S override for tuning).
+// whose rings fit a shared-memory budget of ~220 KB / occ_target CTAs (5 by default: a
+// shallower ring for up to 20 warps per SM; HELM_MARCH_OCC / HELM_MARCH_S override for tuning).
 template <typename R, int MODE, int NV>
 void run_march(MarchArgs<R>& a, cudaStream_t st) {
   auto kern = k_march2d<R, MODE, NV>;
   constexpr int SB = MarchShape<R, MODE, NV>::stage_bytes;
   const size_t zbytes = ((size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>) + 15) / 16 * 16;
-  static const int occ_t = std::max(1, env_int("HELM_MARCH_OCC", 4));
+  static const int occ_t = std::max(1, env_int("HELM_MARCH_OCC", 5));   // bench A/B: 5 vs 4 = +3-5 % (march2d_variants_ab.txt)
   static const int s_fix = env_int("HELM_MARCH_S", 0);
   int S = s_fix >= 3 ? s_fix : (int)(((220 * 1024) / occ_t - (long long)zbytes) / (4 * SB));
   S = std::max(3, std::min(S, 16));
