@@ -184,6 +184,20 @@ helm_status fwi_gn_hessian(const helm_grid* grid, const double* m_slowness2, int
                            int32_t max_rhs, double* h_dev, helm_solve_report* report_host,
                            void* cuda_stream);
 
+/* Batch-mode subset ("a set of source-frequency indices"):
+ * fwi_misfit_grad over only the (frequency, source) pairs with pair_mask[f][s] != 0 (host
+ * uint8 [nfreq][nsrc_total]; sources outside [src_begin, src_end) are ignored), evaluated in
+ * joint batches in frequency-major order. report_host: NULL or [selected pairs][2] in that
+ * order. An empty selection gives f = 0, g = 0. */
+helm_status fwi_misfit_grad_subset(const helm_grid* grid, const double* m_slowness2, int32_t nfreq,
+                                   const double* freq_hz, const double* src_weight_reim,
+                                   int32_t nsrc_total, int32_t src_begin, int32_t src_end,
+                                   const int64_t* src_node, int32_t nrec, const int64_t* rec_node,
+                                   const double* d_obs_reim, const uint8_t* pair_mask,
+                                   const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts,
+                                   int32_t max_rhs, double* fg_dev, helm_solve_report* report_host,
+                                   void* cuda_stream);
+
 /* ---- off-grid acquisition (helm_acq above): Listing 1 OBJ and FORW_MODEL with interpolated
  * P_s, P_r. Same arguments and outputs as fwi_misfit_grad / fwi_forward with the node-id
  * arrays replaced by `acq` (nsrc_total = number of source points, nrec = receiver points);

@@ -77,6 +77,9 @@ SIGNATURES = {
     "fwi_gn_hessian": (C.c_int, [C.POINTER(HelmGrid), _d, C.c_int32, _d, _d, C.c_int32, C.c_int32, _i64,
                                  C.c_int32, _i64, _d, C.POINTER(HelmPml), C.c_int, C.POINTER(HelmSolveOpts),
                                  C.c_int32, _P, _rep, _P]),
+    "fwi_misfit_grad_subset": (C.c_int, [C.POINTER(HelmGrid), _d, C.c_int32, _d, _d, C.c_int32, C.c_int32, C.c_int32,
+                                         _i64, C.c_int32, _i64, _d, C.POINTER(C.c_uint8), C.POINTER(HelmPml), C.c_int,
+                                         C.POINTER(HelmSolveOpts), C.c_int32, _P, _rep, _P]),
     "fwi_misfit_grad_acq": (C.c_int, [C.POINTER(HelmGrid), _d, C.c_int32, _d, _d, C.c_int32, C.c_int32, C.c_int32,
                                       C.c_int32, C.POINTER(HelmAcq), _d, C.POINTER(HelmPml), C.c_int,
                                       C.POINTER(HelmSolveOpts), C.c_int32, _P, _rep, _P]),

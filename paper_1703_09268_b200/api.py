@@ -334,6 +334,33 @@ def fwi_gn_hessian(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], 
     return out, [rep[i].as_dict() for i in range(nrep)]
 
 
+def fwi_misfit_grad_subset(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], src_node: np.ndarray,
+                           rec_node: np.ndarray, d_obs: np.ndarray, pair_mask: np.ndarray, pml: Pml, dtype: int = C128,
+                           opts: SolveOpts = SolveOpts(), max_rhs: int = 16,
+                           src_range: Optional[Tuple[int, int]] = None, weights=None,
+                           fg: Optional[torch.Tensor] = None, stream=None):
+    """Listing 1 `case OBJ` over the (frequency, source) pairs with pair_mask[f, s] (the paper's
+    batch-mode subset): (fg, reports of the selected pairs in frequency-major order)."""
+    lib = L.load()
+    m = np.ascontiguousarray(m_slowness2, np.float64)
+    src = np.ascontiguousarray(src_node, np.int64)
+    rec = np.ascontiguousarray(rec_node, np.int64)
+    d = np.ascontiguousarray(d_obs, np.complex128)
+    f, w = _freq_args(freqs, weights)
+    mask = np.ascontiguousarray(pair_mask, np.uint8).reshape(len(f), len(src))
+    s0, s1 = (0, len(src)) if src_range is None else src_range
+    if fg is None:
+        fg = torch.empty(1 + grid.n_interior, dtype=torch.float64, device="cuda")
+    nrep = int(mask[:, s0:s1].astype(bool).sum()) * 2
+    rep = (L.HelmSolveReport * max(nrep, 1))()
+    g, p, so = grid.c(), pml.c(), opts.c()
+    L.check(lib.fwi_misfit_grad_subset(C.byref(g), _dptr(m), len(f), _dptr(f), None if w is None else _dptr(w), len(src),
+                                       s0, s1, _i64ptr(src), len(rec), _i64ptr(rec), _dp(d),
+                                       mask.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(p), dtype, C.byref(so),
+                                       max_rhs, _tptr(fg), rep, _stream(stream)))
+    return fg, [rep[i].as_dict() for i in range(nrep)]
+
+
 def fwi_misfit_grad_acq(grid: Grid, m_slowness2: np.ndarray, freqs: Sequence[float], acq: Acq, d_obs: np.ndarray,
                         pml: Pml, dtype: int = C128, opts: SolveOpts = SolveOpts(), max_rhs: int = 16,
                         src_range: Optional[Tuple[int, int]] = None, weights=None,

@@ -1380,7 +1380,8 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
              const double* dobs /* OBJ: d_obs, JACADJ: y; host [nfreq][nsrc_total][nrec] */,
              const double* dm /* JAC, GN: host interior */, const helm_solve_opts& so, double* out /* OBJ: [f|g],
              JACADJ/GN: g */, helm_solve_report* rep, double* d_out /* FORW, JAC: host [nfreq][ns][nrec] */,
-             cudaStream_t st, const helm_acq* acq = nullptr /* off-grid points instead of src / rec nodes */) {
+             cudaStream_t st, const helm_acq* acq = nullptr /* off-grid points instead of src / rec nodes */,
+             const uint8_t* mask = nullptr /* [nfreq][nsrc_total]: the (frequency, source) pairs to evaluate */) {
   using C = cx<R>;
   FwiBufs fb;
   const long long N = op->lev[0].N;
@@ -1465,10 +1466,17 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
   std::vector<double> w2_h(B), wop;
   std::vector<long long> srcb_h(B);
   std::vector<int> rop_h(B), fi_h(B), si_h(B);
-  const long long npairs = (long long)nfreq * ns;
-  auto put_rep = [&](int nb, int k) {
+  // the (frequency, source) pairs of this call, frequency-major: all of this shard's, or the
+  // ones `mask` selects (the paper's batch-mode subset interface)
+  std::vector<int> pf, ps;
+  for (int f = 0; f < nfreq; ++f)
+    for (int s = 0; s < ns; ++s)
+      if (!mask || mask[(size_t)f * nsrc_total + s_begin + s]) { pf.push_back(f); ps.push_back(s); }
+  const long long npairs = (long long)pf.size();
+  long long p0 = 0;
+  auto put_rep = [&](int nb, int k) {   // reports in pair order
     if (rep)
-      for (int b = 0; b < nb; ++b) rep[((size_t)fi_h[b] * ns + si_h[b]) * rs + k] = rtmp[b];
+      for (int b = 0; b < nb; ++b) rep[(size_t)(p0 + b) * rs + k] = rtmp[b];
   };
   auto gather_out = [&](int nb, const void* Ufield) {   // d_out[f][s][:] = P_r field
     if (!nrec) return;
@@ -1485,13 +1493,13 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
     for (int b = 0; b < nb; ++b)
       std::memcpy(d_out + 2 * (((size_t)fi_h[b] * ns + si_h[b]) * nrec), &dbat[(size_t)b * nrec], sizeof(double2) * nrec);
   };
-  for (long long p0 = 0; p0 < npairs; p0 += B) {
+  for (p0 = 0; p0 < npairs; p0 += B) {
     const int nb = (int)std::min<long long>(B, npairs - p0);
     // the batch's operators (distinct frequencies, in order) and per-RHS data
     wop.clear();
     int last_f = -1;
     for (int b = 0; b < nb; ++b) {
-      const int fi = (int)((p0 + b) / ns), si = (int)((p0 + b) % ns);
+      const int fi = pf[p0 + b], si = ps[p0 + b];
       if (fi != last_f) { wop.push_back(2.0 * M_PI * freq[fi]); last_f = fi; }
       fi_h[b] = fi; si_h[b] = si; rop_h[b] = (int)wop.size() - 1;
       const double2 S = sw ? make_double2(sw[2 * fi], sw[2 * fi + 1]) : make_double2(1.0, 0.0);
@@ -1725,7 +1733,7 @@ static helm_status fwi_common(FwiMode mode, const helm_grid* grid, const double*
                               const int64_t* src, int32_t nrec, const int64_t* rec, const double* dobs,
                               const double* dm, const helm_pml* pml, helm_dtype dtype, const helm_solve_opts* opts,
                               int32_t max_rhs, double* out, helm_solve_report* rep, double* d_out, void* stream,
-                              const helm_acq* acq = nullptr) {
+                              const helm_acq* acq = nullptr, const uint8_t* mask = nullptr) {
   return wrap([&] {
     validate_grid(grid);
     REQ(m && freq && pml && (src || acq), HELM_ERR_ARG, "NULL argument");
@@ -1753,10 +1761,10 @@ static helm_status fwi_common(FwiMode mode, const helm_grid* grid, const double*
     }
     if (dtype == HELM_C128)
       fwi_run<double>(op, *grid, mode, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, dm, so, out,
-                      rep, d_out, st, acq);
+                      rep, d_out, st, acq, mask);
     else
       fwi_run<float>(op, *grid, mode, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, dm, so, out,
-                     rep, d_out, st, acq);
+                     rep, d_out, st, acq, mask);
   });
 }
 
@@ -1776,6 +1784,17 @@ helm_status fwi_forward(const helm_grid* grid, const double* m, int32_t nfreq, c
   if (!d_host) { g_err = "d_host is NULL"; return HELM_ERR_ARG; }
   return fwi_common(FW_FORW, grid, m, nfreq, freq, sw, s_end, s_begin, s_end, src, nrec, rec, nullptr, nullptr, pml,
                     dtype, opts, max_rhs, nullptr, rep, d_host, stream);
+}
+
+helm_status fwi_misfit_grad_subset(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq,
+                                   const double* sw, int32_t nsrc_total, int32_t s_begin, int32_t s_end,
+                                   const int64_t* src, int32_t nrec, const int64_t* rec, const double* dobs,
+                                   const uint8_t* pair_mask, const helm_pml* pml, helm_dtype dtype,
+                                   const helm_solve_opts* opts, int32_t max_rhs, double* fg, helm_solve_report* rep,
+                                   void* stream) {
+  if (!pair_mask) { g_err = "pair_mask is NULL"; return HELM_ERR_ARG; }
+  return fwi_common(FW_OBJ, grid, m, nfreq, freq, sw, nsrc_total, s_begin, s_end, src, nrec, rec, dobs, nullptr, pml,
+                    dtype, opts, max_rhs, fg, rep, nullptr, stream, nullptr, pair_mask);
 }
 
 helm_status fwi_misfit_grad_acq(const helm_grid* grid, const double* m, int32_t nfreq, const double* freq,
