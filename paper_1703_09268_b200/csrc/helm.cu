@@ -467,7 +467,9 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
   auto kern = k_march2d<R, MODE, NV>;
   constexpr int SB = MarchShape<R, MODE, NV>::stage_bytes;
   const size_t zbytes = ((size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>) + 15) / 16 * 16;
-  static const int occ_t = std::max(1, env_int("HELM_MARCH_OCC", 5));   // bench A/B: 5 vs 4 = +3-5 % (march2d_variants_ab.txt)
+  // bench A/B (march2d_variants_ab.txt): complex128 5 vs 4 = +3-5 %; complex64 (half the stage
+  // bytes) 8 vs 5 = +8 % on the level-1 fused steps
+  static const int occ_t = std::max(1, env_int("HELM_MARCH_OCC", sizeof(R) == 4 ? 8 : 5));
   static const int s_fix = env_int("HELM_MARCH_S", 0);
   int S = s_fix >= 3 ? s_fix : (int)(((220 * 1024) / occ_t - (long long)zbytes) / (4 * SB));
   S = std::max(3, std::min(S, 16));
