@@ -6,6 +6,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <tuple>
 #include <cmath>
 #include <cstdio>
@@ -59,7 +60,7 @@ struct Prof {
   bool cur_sampled = false;
 };
 Prof g_prof;
-long long g_launches = 0;
+std::atomic<long long> g_launches{0};   // all threads (fwi evaluations may run concurrently)
 
 cudaEvent_t prof_event() {
   if (!g_prof.pool.empty()) {
@@ -475,8 +476,8 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
   S = std::max(3, std::min(S, 16));
   const size_t smem = zbytes + (size_t)4 * S * SB;
   struct Cfg { size_t smem = 0; int occ = 0; };
-  static Cfg cache[4];   // small cache of (smem -> occupancy)
-  static size_t attr_max = 48 * 1024;   // the opt-in limit only ever grows
+  thread_local Cfg cache[4];   // small per-thread cache of (smem -> occupancy)
+  thread_local size_t attr_max = 48 * 1024;   // the opt-in limit only ever grows
   if (smem > attr_max) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_max = smem;
@@ -487,7 +488,7 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
   if (!occ) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem));
     if (occ < 1) throw HelmErr{HELM_ERR_STATE, "march kernel does not fit on an SM"};
-    static int next = 0;
+    thread_local int next = 0;
     cache[next] = Cfg{smem, occ};
     next = (next + 1) % 4;
     if (env_int("HELM_DEBUG", 0)) {
