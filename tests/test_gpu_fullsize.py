@@ -6,7 +6,9 @@
 * cfg3 (configs[2]): 64^3 + PML 10 preconditioned solve — true residual certified by the
   oracle's own assembled H (<= 1e-6), analytic -e^{ikr}/(4 pi r) within 15 % (STD2 at 12.5
   points per wavelength, SURVEY c.4), and the 8-source batch.
-* cfg4 (configs[3]) replica at 24^3 from the same generator: f, g vs oracle LU.
+* cfg4 (configs[3]) replica at 24^3 from the same generator: f, g vs oracle LU; and at full
+  size (220^3 extended) one solve whose residual, recomputed by the oracle's rows of H on
+  sampled z-slabs, is bounded by the certified 1e-6.
 * cfg5 (configs[4]) 256^3 matvec, c128 and c64, batch 4, forward and adjoint: sampled
   z-slabs vs the oracle's slab rows of H (c128 <= 1e-12, c64 <= 1e-5).
 Every expected value comes from oracle/ (LU, sparse rows) or closed forms.
@@ -143,3 +145,32 @@ def test_table3_smallest_cell_certified():
     rep = api.helm_solve(op, to_dev(q), x)
     H = D.helmholtz_matrix(p, w, D.PmlParams(v_ref=2000.0))
     assert rep[0]["converged"] and rel_residual(H, to_host(x)[0], q) <= 1e-6 * (1 + 1e-3)
+
+
+def test_cfg4_fullsize_solve_sampled_residual():
+    """cfg4 (configs[3]) at full size (200^3 + PML 10, 6 Hz, c128, bench-like preconditioned
+    solve): the residual q - H u recomputed by the oracle's own rows of H on sampled z-slabs
+    (the source slab, PML slabs and random interior ones) is bounded by the solver's certified
+    global residual: sqrt(sum_slabs ||r_slab||^2) <= ||r|| <= 1e-6 ||q||."""
+    p = synth.cfg4()
+    w = 2 * np.pi * p.freqs[0]
+    pml = D.PmlParams(v_ref=4500.0)
+    op = api.helm_setup(api.Grid.of(p), p.m, w, api.Pml(v_ref=4500.0), api.C128, max_rhs=1)
+    q = fwi.source_matrix(p, w, p.src[:1])[:, 0]
+    x = torch.zeros(1, p.n_ext, dtype=torch.complex128, device="cuda")
+    rep = api.helm_solve(op, to_dev(q), x)
+    assert rep[0]["converged"] and rep[0]["rel_residual"] <= 1e-6
+    u = to_host(x)[0]
+    del op, x
+    Nx, Ny, Nz = p.next
+    plane = Nx * Ny
+    zs = int(p.src[0]) // (p.n[0] * p.n[1]) + p.pml[2][0]
+    rng = np.random.default_rng(5)
+    slabs = sorted({0, Nz - 2, max(zs - 1, 0)} | set(rng.choice(np.arange(2, Nz - 4), 5, replace=False).tolist()))
+    ss = 0.0
+    for z0 in slabs:
+        rows = D.helmholtz_rows(p, w, pml, z0, z0 + 2)
+        r = q[z0 * plane:(z0 + 2) * plane] - rows @ u
+        ss += float(np.vdot(r, r).real)
+    assert np.sqrt(ss) <= 1e-6 * np.linalg.norm(q) * (1 + 1e-3)
+    assert np.sqrt(ss) > 0.0
