@@ -11,6 +11,7 @@
   sampled z-slabs, is bounded by the certified 1e-6.
 * cfg5 (configs[4]) 256^3 matvec, c128 and c64, batch 4, forward and adjoint: sampled
   z-slabs vs the oracle's slab rows of H (c128 <= 1e-12, c64 <= 1e-5).
+* cfg2 at full size, joint batch of 150: J^H y and the Gauss-Newton product vs oracle LU.
 Every expected value comes from oracle/ (LU, sparse rows) or closed forms.
 """
 import numpy as np
@@ -174,3 +175,22 @@ def test_cfg4_fullsize_solve_sampled_residual():
         ss += float(np.vdot(r, r).real)
     assert np.sqrt(ss) <= 1e-6 * np.linalg.norm(q) * (1 + 1e-3)
     assert np.sqrt(ss) > 0.0
+
+
+def test_cfg2_full_gn_hessian_and_jacobian_adjoint_match_oracle():
+    """SURVEY §8(f) rank 1 at configs[1]'s full size, in the bench's launch configuration (one
+    joint batch of all 150 (source, frequency) pairs): J^H y and the Gauss-Newton product
+    J^H J dm vs the oracle's LU evaluation (solves to 1e-8, tolerance 1e-6)."""
+    p = synth.cfg2()
+    pml = D.PmlParams(v_ref=VREF2)
+    rng = np.random.default_rng(11)
+    dm = 0.05 * np.abs(p.m).max() * rng.standard_normal(p.m.shape)
+    sh = (len(p.freqs), len(p.src), len(p.rec))
+    y = rng.standard_normal(sh) + 1j * rng.standard_normal(sh)
+    a = dict(grid=api.Grid.of(p), freqs=p.freqs, src_node=p.src, rec_node=p.rec, pml=api.Pml(v_ref=VREF2),
+             dtype=api.C128, opts=api.SolveOpts(rtol=1e-8), max_rhs=150)
+    h, rep = api.fwi_gn_hessian(m_slowness2=p.m, dm=dm, **a)
+    assert len(rep) == 450 and all(r["converged"] for r in rep)
+    assert rel(h.cpu().numpy(), fwi.gn_hessian(p, pml, dm, p.m).ravel()) <= 1e-6
+    g, _ = api.fwi_jacobian_adjoint(m_slowness2=p.m, y=y, **a)
+    assert rel(g.cpu().numpy(), fwi.jacobian_adjoint(p, pml, y, p.m).ravel()) <= 1e-6
