@@ -1,14 +1,17 @@
 #!/usr/bin/env python
 """bench.py — one JSON line for the driver.
 
-A step = one full pass of the hot path: fwi_misfit_grad over this
-rank's shots of BASELINE configs[1] (2D FWI, 401x201 + PML 20, 50 shots x 3 frequencies,
-401 receivers) = 300 preconditioned solves (150 forward + 150 adjoint), then one NCCL
-all_reduce of [f || g]. Weak scaling: rank r fires its own 50 shots (x = 4 + 8k + r), so the
-per-GPU work is fixed as N grows; at N = 1 the workload is exactly configs[1].
+A step = one full pass of the hot path on BASELINE configs[3] (cfg4,
+the configuration the metric's "preconditioned solves/s per GPU at 1/2/4/8" is quoted on):
+fwi_misfit_grad over this rank's 8-source shard of the 64-source survey through
+dist.misfit_grad_sharded = 16 preconditioned solves (8 forward + 8 adjoint) on the 220^3
+extended grid, then ONE in-place fp64 NCCL all_reduce of [f || g] when N > 1. Weak scaling:
+the survey at N GPUs is the first 8 N sources (N = 8: all 64). `value` = solves/s over all
+ranks. Secondary keys at N = 1: the other dtype, cfg2 (configs[1]) and the whole configs[4]
+matvec sweep.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--dtype c128|c64] [--workload cfg2|cfg3]
+                    [--dtype c128|c64] [--workload cfg4|cfg2|cfg3]
 """
 from __future__ import annotations
 
@@ -40,19 +43,40 @@ def peaks():
 
 
 # ----------------------------------------------------------------------------- workload
-def workload(name: str, rank: int):
+CFG4_SHARD = 8   # sources per rank and step: at N = 8 the step is the whole 64-source cfg4 survey
+
+
+def workload(name: str, rank: int, size: int):
+    """(problem with the survey's sources, this rank's source range, description, PML v_ref, max_rhs).
+
+    cfg4 (BASELINE configs[3], the metric's "preconditioned solves/s per GPU at 1/2/4/8"): the
+    survey at N GPUs is the first 8 N of the 64 surface sources; rank r owns [8 r, 8 r + 8) via
+    dist.shard (weak scaling: 16 solves per rank and step; at N = 8 it is the full survey).
+    cfg2 (configs[1]): each rank fires its own 50 shots (x = 4 + 8k + r mod 4 stays inside the
+    401-point interior), all three frequencies."""
     import synth
+    from paper_1703_09268_b200 import dist as hdist
+    if name == "cfg4":
+        p = synth.cfg4()
+        ns = min(64, CFG4_SHARD * size)
+        p = p.with_(src=p.src[:ns])
+        s0, s1 = hdist.shard(ns, rank, size)
+        desc = ("cfg4 (BASELINE configs[3]): 3D layered 1500-4500 m/s + 5%% smoothed noise, 200^3 interior + PML %d "
+                "(%d^3 ext, %.1f M points), h=25 m, f=6 Hz, 40,000 surface receivers; survey = first %d of the 64 "
+                "surface sources, %d per GPU (dist.shard), misfit+gradient"
+                % (p.pml[0][0], p.next[0], p.n_ext / 1e6, ns, s1 - s0))
+        return p, (s0, s1), desc, 4500.0, s1 - s0
     if name == "cfg2":
         p = synth.cfg2()
         n = p.n
-        src = synth.node_id(4 + 8 * np.arange(50) + (rank % 8), 0, 2, n)
+        src = synth.node_id(4 + 8 * np.arange(50) + (rank % 4), 0, 2, n)
         desc = ("cfg2 (BASELINE configs[1]): 2D FWI misfit+gradient, 401x201 interior + PML 20 "
                 "(441x241 ext), h=10 m, v 1500-4000 m/s + 8 seeded blobs, 50 shots x {3,5,7} Hz, 401 receivers")
-        return p.with_(src=src), desc, 3000.0 * 1.0
+        return p.with_(src=src), (0, 50), desc, 3000.0, 150
     if name == "cfg3":
         p = synth.cfg3_batch(8)
-        desc = "cfg3 batch: 3D constant 64^3 + PML 10 (84^3 ext), 8 sources, f=8 Hz (forward solves only)"
-        return p, desc, 2000.0
+        desc = "cfg3 batch: 3D constant 64^3 + PML 10 (84^3 ext), 8 sources, f=8 Hz"
+        return p, (0, 8), desc, 2000.0, 8
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -105,54 +129,66 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- our arm
-def run_ours(args, rank, size, dev):
+KERNEL_DESC = {"arnoldi": "fused GMRES Arnoldi step (form v_j + stencil + projections + norm; k_plane MODE 3/4 in 3D, "
+                          "k_march2d MODE 3/4 in 2D)",
+               "solupdate": "solution update x += sum y_i z_i (k_solupdate_t)",
+               "stencil_resid": "residual r = b - Hx + norm (stencil MODE 1)",
+               "stencil": "FGMRES stencil + projections (MODE 2)"}
+
+
+def evaluate_workload(name, args, rank, size, dtype, steps, warmup, profile=True, e2e=True, clocks=True):
+    """Time `steps` misfit+gradient evaluations of workload `name` (after `warmup`), each through
+    dist.misfit_grad_sharded (this rank's source shard, then ONE in-place fp64 all_reduce of
+    [f || g] when N > 1). Returns a dict of the measured quantities."""
     import torch
     import torch.distributed as dist
 
     from paper_1703_09268_b200 import api
     from paper_1703_09268_b200 import dist as hdist
 
-    prob, desc, vref = workload(args.workload, rank)
-    dtype = api.C64 if args.dtype == "c64" else api.C128
+    prob, (s0, s1), desc, vref, max_rhs = workload(name, rank, size)
+    if args.max_rhs > 0:
+        max_rhs = args.max_rhs
     grid = api.Grid.of(prob)
     pml = api.Pml(v_ref=vref)
     opts = api.SolveOpts(rtol=1e-6)
     nsrc = len(prob.src)
-    # joint (source, frequency) batches: by default one batch holds every pair
-    max_rhs = args.max_rhs if args.max_rhs > 0 else nsrc * len(prob.freqs)
+    nf = len(prob.freqs)
     stream = torch.cuda.current_stream()
 
-    # observed data from the true model (untimed): Listing 1 FORW_MODEL on this rank's shots
-    d_obs, _ = api.fwi_forward(grid, prob.m_true, prob.freqs, prob.src, prob.rec, pml, api.C128,
-                               api.SolveOpts(rtol=1e-8), max_rhs=max_rhs)
+    # observed data at the true model (untimed): Listing 1 FORW_MODEL on this rank's shard at
+    # rtol 1e-8; the other ranks' rows stay zero (fwi_misfit_grad reads its own shard only)
+    d_obs = np.zeros((nf, nsrc, len(prob.rec)), np.complex128)
+    d_sh, _ = api.fwi_forward(grid, prob.m_true, prob.freqs, prob.src, prob.rec, pml, api.C128,
+                              api.SolveOpts(rtol=1e-8), max_rhs=max_rhs, src_range=(s0, s1))
+    d_obs[:, s0:s1] = d_sh
     fg = torch.empty(1 + grid.n_interior, dtype=torch.float64, device="cuda")
 
-    def step(fg_out, host_roundtrip=False):
-        fg2, rep = api.fwi_misfit_grad(grid, prob.m, prob.freqs, prob.src, prob.rec, d_obs, pml, dtype, opts,
-                                       max_rhs=max_rhs, fg=fg_out)
-        if size > 1:
-            dist.all_reduce(fg2, op=dist.ReduceOp.SUM)
+    def step(host_roundtrip=False):
+        fg2, rep, _ = hdist.misfit_grad_sharded(nsrc=nsrc, grid=grid, m_slowness2=prob.m, freqs=prob.freqs,
+                                                src_node=prob.src, rec_node=prob.rec, d_obs=d_obs, pml=pml,
+                                                dtype=dtype, opts=opts, max_rhs=max_rhs, fg=fg)
         if host_roundtrip:
             return fg2.cpu(), rep
         return fg2, rep
 
-    reps = None
-    for _ in range(args.warmup):
-        _, reps = step(fg)
-    solves_per_step = 2 * nsrc * len(prob.freqs)
+    for _ in range(warmup):
+        step()
+    solves_per_rank = 2 * (s1 - s0) * nf
 
-    def timed(k, host_roundtrip=False, profile=False):
+    def timed(k, host_roundtrip=False, prof=False):
         if size > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        if profile:
+        if prof:
             api.profile(True, args.probe_stride)
         l0 = api.launch_count()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        rep = None
+        reps = []
         for _ in range(k):
-            _, rep = step(fg, host_roundtrip)
+            _, rep = step(host_roundtrip)
+            reps.append(rep)
         e1.record(stream)
         torch.cuda.synchronize()
         launches = api.launch_count() - l0
@@ -162,51 +198,54 @@ def run_ours(args, rank, size, dev):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
             dist.barrier()
-        return ms, launches, rep
+        return ms, launches, reps
 
-    with ClockSampler(dev) as clk:
-        ms, launches, reps = timed(args.steps)
-    # kernel-class shares and the live roofline of the dominant class: one more step with
-    # every `probe_stride`-th launch bracketed by CUDA events (not part of `value`)
-    timed(1, profile=True)
-    prof = api.profile_read()
-    prof_lv = {lv: api.profile_read(lv) for lv in range(4)}
-    api.profile(False, 1)
-    ms_e2e, _, _ = timed(max(1, min(args.steps, 2)), host_roundtrip=True)
-    k_e2e = max(1, min(args.steps, 2))
+    if clocks:
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            ms, launches, reps = timed(steps)
+        clk_sum = clk.summary()
+    else:
+        ms, launches, reps = timed(steps)
+        clk_sum = None
+    # solves over all ranks: every rank's shard size is the same (8 for cfg4)
+    value = solves_per_rank * size * steps / (ms / 1e3)
+    res = {"prob": prob, "grid": grid, "desc": desc, "max_rhs": max_rhs, "nsrc": nsrc, "shard": (s0, s1),
+           "value": value, "ms": ms, "steps": steps, "launches": launches, "reps": reps, "clocks": clk_sum,
+           "solves_per_rank": solves_per_rank, "d_obs_shard_bytes": int(d_sh.nbytes)}
+    if profile:
+        # kernel-class shares and the live roofline of the dominant class: one more step with
+        # every `probe_stride`-th launch bracketed by CUDA events on the launch stream
+        timed(1, prof=True)
+        res["prof"] = api.profile_read()
+        res["prof_lv"] = {lv: api.profile_read(lv) for lv in range(4)}
+        api.profile(False, 1)
+    if e2e:
+        k_e2e = max(1, min(steps, 2))
+        ms_e2e, _, _ = timed(k_e2e, host_roundtrip=True)
+        res["e2e_value"] = solves_per_rank * size * k_e2e / (ms_e2e / 1e3)
+    return res
 
-    value = solves_per_step * size * args.steps / (ms / 1e3)
-    e2e_value = solves_per_step * size * k_e2e / (ms_e2e / 1e3)
-    hbm, peak_kind = peaks()
 
-    # shares of device time per kernel class, and the dominant (class, level) pair: its live
-    # roofline is algorithmic bytes / event-timed duration over its sampled launches
-    est = {}
-    for name, p in prof.items():
-        if p["sampled"]:
-            est[name] = p["ms"] * p["launches"] / p["sampled"]
-    total_est = sum(est.values()) or 1.0
-    kernel_shares = {k: round(v / total_est, 3) for k, v in sorted(est.items(), key=lambda kv: -kv[1])}
-    cl = {}
-    for lv, pr in prof_lv.items():
-        for name, p in pr.items():
-            if p["sampled"]:
-                cl[(name, lv)] = p
+def roofline_from_profile(res, hbm, peak_kind, workload_name):
+    prof, prof_lv = res["prof"], res["prof_lv"]
+
     def est_ms(p):
         return p["ms"] * p["launches"] / p["sampled"]
-    roof = None
+    est = {name: est_ms(p) for name, p in prof.items() if p["sampled"]}
+    total_est = sum(est.values()) or 1.0
+    kernel_shares = {k: round(v / total_est, 3) for k, v in sorted(est.items(), key=lambda kv: -kv[1])}
+    cl = {(name, lv): p for lv, pr in prof_lv.items() for name, p in pr.items() if p["sampled"]}
     level_shares = {}
     for (name, lv), p in cl.items():
-        level_shares.setdefault(f"L{lv}", 0.0)
-        level_shares[f"L{lv}"] += est_ms(p) / total_est
+        level_shares[f"L{lv}"] = level_shares.get(f"L{lv}", 0.0) + est_ms(p) / total_est
     level_shares = {k: round(v, 3) for k, v in sorted(level_shares.items())}
+    roof = None
     if cl:
         (dname, dlv), p = max(cl.items(), key=lambda kv: est_ms(kv[1]))
         achieved = p["bytes"] / (p["ms"] / 1e3) / 1e9
-        tr = traffic_for(f"{dname}@L{dlv}")
-        roof = {"kernel": f"{dname} (fused GMRES Arnoldi step, k_march2d MODE 3/4) at level {dlv}" if dname == "arnoldi"
-                else f"{dname} at level {dlv}", "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-                "unit": "GB/s", "frac": round(achieved / hbm, 4),
+        tr = traffic_for(f"{workload_name}:{dname}@L{dlv}")
+        roof = {"kernel": f"{KERNEL_DESC.get(dname, dname)} at level {dlv}", "bound": "hbm",
+                "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                 "traffic": round(tr["ratio"] * p["bytes"] / p["sampled"]) if tr else None,
                 "traffic_note": tr.get("note") if tr else None,
                 "peak_kind": peak_kind, "share_of_step": round(est_ms(p) / total_est, 3),
@@ -215,36 +254,54 @@ def run_ours(args, rank, size, dev):
         cls_all = prof[dname]
         roof["class_all_levels"] = {"achieved": round(cls_all["bytes"] / (cls_all["ms"] / 1e3) / 1e9, 1),
                                     "share_of_step": kernel_shares.get(dname)}
+    return roof, kernel_shares, level_shares
 
-    cycles = [r["outer_cycles"] for r in (reps or [])]
+
+def run_ours(args, rank, size, dev):
+    from paper_1703_09268_b200 import api
+
+    dtype = api.C64 if args.dtype == "c64" else api.C128
+    res = evaluate_workload(args.workload, args, rank, size, dtype, args.steps, args.warmup)
+    hbm, peak_kind = peaks()
+    roof, kernel_shares, level_shares = roofline_from_profile(res, hbm, peak_kind, args.workload)
+    reps = [r for rr in res["reps"] for r in rr]
+    cycles = [r["outer_cycles"] for r in res["reps"][-1]]
+    nsh = res["shard"][1] - res["shard"][0]
+    fwd_cyc = [r["outer_cycles"] for i, r in enumerate(res["reps"][-1]) if i % 2 == 0]
+    adj_cyc = [r["outer_cycles"] for i, r in enumerate(res["reps"][-1]) if i % 2 == 1]
     # whole-step algorithmic HBM bytes counted by the library (every executed kernel, SURVEY d.2)
-    step_bytes = sum(r["bytes_alg"] for r in (reps or []))
-    solve_roof = {"alg_bytes_per_step": step_bytes, "achieved_GBps": round(step_bytes / (ms / args.steps / 1e3) / 1e9, 1),
-                  "frac": round(step_bytes / (ms / args.steps / 1e3) / 1e9 / peaks()[0], 4)}
-    h2d = 8 * grid.n_interior + 16 * d_obs.size + 8 * (nsrc + len(prob.rec)) + 16 * len(prob.freqs)
+    step_bytes = sum(r["bytes_alg"] for r in res["reps"][-1])
+    ms = res["ms"]
+    solve_roof = {"alg_bytes_per_step": step_bytes,
+                  "achieved_GBps": round(step_bytes / (ms / args.steps / 1e3) / 1e9, 1),
+                  "frac": round(step_bytes / (ms / args.steps / 1e3) / 1e9 / hbm, 4)}
+    grid, prob = res["grid"], res["prob"]
+    h2d = 8 * grid.n_interior + res["d_obs_shard_bytes"] + 8 * (len(prob.src) + len(prob.rec)) + 16 * len(prob.freqs)
     d2h = 8 * (1 + grid.n_interior)
     out = {
-        "metric": METRIC, "value": round(value, 3), "unit": "solves/s", "n_gpus": size, "steps": args.steps,
+        "metric": METRIC, "value": round(res["value"], 4), "unit": "solves/s", "n_gpus": size, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "c128" if dtype == api.C128 else "c64 (mixed: c128 outer FGMRES)",
         "data": "synthetic (seeded generators, synth/)",
-        "config": {"workload": desc, "solves_per_step_per_gpu": solves_per_step, "rtol": opts.rtol,
-                   "precond": "ML-GMRES (3,5,3,5), 3 grids, outer FGMRES(5)", "max_rhs": max_rhs,
-                   "batching": "joint (source, frequency) batches of max_rhs RHS (P:141)",
-                   "l2": "no flush: working set %.1f GB > 126 MB L2" % (ws_bytes(grid, dtype, max_rhs) / 1e9),
-                   "parallelism": f"dp{size} (source shards, one fp64 NCCL all_reduce per step)",
-                   "outer_cycles_last_step": {"min": min(cycles), "max": max(cycles)} if cycles else None},
-        "e2e": {"value": round(e2e_value, 3), "unit": "solves/s", "h2d_bytes_per_step": h2d,
+        "config": {"workload": res["desc"], "solves_per_step_per_gpu": res["solves_per_rank"], "rtol": 1e-6,
+                   "precond": "ML-GMRES (3,5,3,5), 3 grids, outer FGMRES(5)", "max_rhs": res["max_rhs"],
+                   "batching": "the rank's (source, frequency) pairs in joint batches of max_rhs RHS (P:141)",
+                   "l2": "no flush: working set %.1f GB > 126 MB L2" % (ws_bytes(grid, dtype, res["max_rhs"]) / 1e9),
+                   "parallelism": f"dp{size} (dist.misfit_grad_sharded: source shards, one fp64 NCCL all_reduce "
+                                  "of [f||g] per step)",
+                   "outer_cycles_last_step": {"forward": fwd_cyc, "adjoint": adj_cyc,
+                                              "mean": round(float(np.mean(cycles)), 2)} if cycles else None},
+        "e2e": {"value": round(res["e2e_value"], 4), "unit": "solves/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": int(launches),
+        "gpu_launches": int(res["launches"]),
         "roofline": roof,
         "kernel_shares": kernel_shares,
         "level_shares": level_shares,
         "solve_roofline": solve_roof,
-        "clocks": clk.summary(),
+        "clocks": res["clocks"],
     }
-    return out, prob
+    return out, res
 
 
 def ws_bytes(grid, dtype, max_rhs):
@@ -264,20 +321,29 @@ def traffic_for(key):
         return None
 
 
+_CFG5 = {}
+
+
 def matvec_probe(dtype_name="c128", N=256, nrhs=1, reps=10):
-    """a2 alone on BASELINE configs[4] (cfg5 N^3): Gpts/s with 3 rotating buffer sets > 2 x L2."""
+    """a2 alone on BASELINE configs[4] (cfg5 N^3): Gpts/s. Between timed launches the input
+    rotates over buffer sets whose total exceeds 2 x L2 (one set when it alone does)."""
     import torch
 
     import synth
     from paper_1703_09268_b200 import api
-    p = synth.cfg5(N)
+    if N not in _CFG5:
+        _CFG5.clear()
+        _CFG5[N] = synth.cfg5(N)
+    p = _CFG5[N]
     dtype = api.C128 if dtype_name == "c128" else api.C64
     op = api.helm_setup(api.Grid.of(p), p.m, 2 * np.pi * 6.0, api.Pml(v_ref=4500.0), dtype, max_rhs=nrhs,
                         mlopts=api.MlOpts(levels=0))   # operator only: no solver workspace
     td = torch.complex128 if dtype == api.C128 else torch.complex64
     g = torch.Generator(device="cuda").manual_seed(1)
     n_ext = p.n_ext
-    sets = max(3, int(np.ceil(2 * 126e6 / (2 * n_ext * nrhs * (16 if dtype == api.C128 else 8)))) + 1)
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    set_bytes = 2 * n_ext * nrhs * (16 if dtype == api.C128 else 8)
+    sets = 1 if set_bytes > 2 * l2 else int(np.ceil(2 * l2 / set_bytes)) + 1
     xs = [torch.randn(nrhs, n_ext, dtype=td, device="cuda", generator=g) for _ in range(sets)]
     ys = [torch.empty_like(xs[0]) for _ in range(sets)]
     for i in range(3):
@@ -291,54 +357,150 @@ def matvec_probe(dtype_name="c128", N=256, nrhs=1, reps=10):
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
+    del xs, ys, op
+    torch.cuda.empty_cache()
     t = statistics.median(times) / 1e3
     sc, sr = (16, 8) if dtype == api.C128 else (8, 4)
     gpts = n_ext * nrhs / t / 1e9
     gbs = n_ext * (2 * sc * nrhs + sr) / t / 1e9
     hbm, _ = peaks()
-    return {"workload": f"cfg5 {N}^3 {dtype_name} b={nrhs}", "gpts": round(gpts, 2), "gb_s": round(gbs, 1),
-            "hbm_frac": round(gbs / hbm, 4), "ms": round(t * 1e3, 4), "best_ms": round(min(times), 4)}
+    return {"gpts": round(gpts, 2), "gb_s": round(gbs, 1), "hbm_frac": round(gbs / hbm, 4),
+            "frac_of_8TBs": round(gbs / 8000.0, 4), "ms": round(t * 1e3, 4), "best_ms": round(min(times), 4),
+            "buffer_sets": sets}
+
+
+def matvec_sweep():
+    """The whole BASELINE configs[4] sweep: N in {128, 256, 384, 512} x {c64, c128} x b in {1, 4, 16}."""
+    out = {}
+    for N in (128, 256, 384, 512):
+        for dt in ("c128", "c64"):
+            for b in (1, 4, 16):
+                out[f"{dt}_b{b}_{N}"] = matvec_probe(dt, N, b)
+    return out
 
 
 # ----------------------------------------------------------------------------- oracle arm
-def oracle_step(prob, d, fi, pml):
-    """One bounded sample of the workload on the host: the oracle's misfit+gradient for one
-    frequency over all shots (LU factorization + forward and adjoint triangular solves)."""
+def host_info():
+    try:
+        model = next(l.split(":", 1)[1].strip() for l in subprocess.run(["lscpu"], capture_output=True, text=True)
+                     .stdout.splitlines() if l.startswith("Model name"))
+    except Exception:
+        model = "unknown"
+    return os.cpu_count() or 1, model
+
+
+def _replica_task(args):
+    """One process of the all-cores oracle baseline: misfit+gradient (LU + forward and adjoint
+    solves) of the cfg4 replica for one source."""
+    s, d_all = args
+    import synth
+    from oracle import discretize as D
     from oracle import fwi
-    p1 = prob.with_(freqs=(prob.freqs[fi],))
+    pr = synth.cfg4_replica(**REPLICA)
+    pml = D.PmlParams(v_ref=4500.0)
     t0 = time.perf_counter()
-    fwi.misfit_grad(p1, pml, d[fi:fi + 1])
-    return time.perf_counter() - t0, 2 * len(prob.src)
+    fwi.misfit_grad(pr, pml, d_all[:, s % len(pr.src):s % len(pr.src) + 1], src_ids=pr.src[s % len(pr.src):s % len(pr.src) + 1])
+    return time.perf_counter() - t0
 
 
-def cpu_baseline(prob, pml_o, d=None):
+# the oracle's bounded sample of cfg4: a replica from the same generator, small enough that its
+# 3D sparse LU takes ~2 s (the 24^3 test replica's LU takes ~17 s per evaluation)
+REPLICA = dict(n=16, pml=4)
+REPLICA_DESC = "cfg4 replica 16^3 + PML 4 (24^3 ext, same generator, 4 sources, 256 receivers, 6 Hz)"
+_REPLICA_D = {}
+
+
+def oracle_replica_step():
+    """One bounded sample of the cfg4 workload for the oracle: its misfit + gradient (LU, forward
+    and adjoint solves of all 4 sources) on the replica; SuperLU, 1 thread. Observed data are
+    computed once (untimed)."""
+    import synth
+    from oracle import discretize as D
     from oracle import fwi
-    if d is None:
-        d = fwi.forward_data(prob.with_(freqs=(prob.freqs[1],)), pml_o, prob.m_true)
-        fi = 0
-        p = prob.with_(freqs=(prob.freqs[1],))
-    else:
-        fi, p = 1, prob
-    dt, n = oracle_step(p, d, fi, pml_o)
-    return {"value": round(n / dt, 4), "unit": "solves/s", "cores": 1, "kind": "oracle",
-            "sample": f"oracle (scipy SuperLU, 1 thread) misfit+gradient of {p.name} at {p.freqs[fi]} Hz over "
-                      f"{len(prob.src)} shots = {n} solves in {dt:.1f} s"}
+    pr = synth.cfg4_replica(**REPLICA)
+    pml = D.PmlParams(v_ref=4500.0)
+    if "d" not in _REPLICA_D:
+        _REPLICA_D["d"] = fwi.forward_data(pr, pml, pr.m_true)
+    d = _REPLICA_D["d"]
+    t0 = time.perf_counter()
+    fwi.misfit_grad(pr, pml, d)
+    return time.perf_counter() - t0, 2 * len(pr.src), d
+
+
+def cpu_baseline_cfg4(alg_bytes_per_solve=None):
+    """The oracle on the GPU box's host (SURVEY d.4): (1) one core, the cfg4 replica's misfit +
+    gradient (LU); (2) all cores, independent single-source replica evaluations in nproc
+    processes; (3) the oracle's SpMV on the FULL cfg4 operator (220^3, assembled CSR), and the
+    EXTRAPOLATED full-size solve rate if the oracle moved the same algorithmic bytes per solve as
+    the GPU path at its SpMV's effective bandwidth (labelled: not a measurement)."""
+    import multiprocessing as mp
+
+    import synth
+    from oracle import discretize as D
+    cores, model = host_info()
+    dt, n, d = oracle_replica_step()
+    ntask = max(cores, 4)
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_replica_task, [(s, d) for s in range(ntask)])
+    wall = time.perf_counter() - t0
+    p = synth.cfg4()
+    t1 = time.perf_counter()
+    H = D.helmholtz_matrix(p, 2 * np.pi * 6.0, D.PmlParams(v_ref=4500.0))
+    t_asm = time.perf_counter() - t1
+    x = np.random.default_rng(1).standard_normal(p.n_ext) + 0j
+    ts = []
+    for _ in range(3):
+        t2 = time.perf_counter()
+        H @ x
+        ts.append(time.perf_counter() - t2)
+    t_spmv = min(ts)
+    spmv_gbs = p.n_ext * (2 * 16 + 8) / t_spmv / 1e9
+    out = {"value": round(n / dt, 4), "unit": "solves/s", "cores": 1, "kind": "oracle",
+           "sample": f"oracle misfit+gradient (scipy SuperLU, 1 thread) on the {REPLICA_DESC}: {n} solves in {dt:.2f} s",
+           "host": {"nproc": cores, "lscpu_model": model},
+           "all_cores": {"value": round(2 * ntask / wall, 4), "unit": "solves/s", "cores": cores,
+                         "sample": f"{ntask} single-source replica misfit+gradient evaluations (LU each) in {cores} "
+                                   f"processes, {wall:.2f} s wall"},
+           "fullsize_spmv": {"workload": "cfg4 220^3 c128, assembled CSR (74.2 M nonzeros), 1 thread",
+                             "gpts": round(p.n_ext / t_spmv / 1e9, 4), "gb_s_alg": round(spmv_gbs, 2),
+                             "ms": round(1e3 * t_spmv, 1), "assembly_s": round(t_asm, 1)}}
+    if alg_bytes_per_solve:
+        t_solve = alg_bytes_per_solve / (spmv_gbs * 1e9)
+        out["extrapolated_fullsize"] = {
+            "value": round(1.0 / t_solve, 6), "unit": "solves/s", "kind": "EXTRAPOLATED, not measured",
+            "how": "GPU path's algorithmic bytes per cfg4 solve / the oracle SpMV's effective algorithmic bandwidth "
+                   "(1 thread)"}
+    return out
 
 
 def run_reference(args, rank, size):
+    """`--impl reference`: the oracle as it stands on the host cores, each step one bounded sample
+    of the headline workload (cfg4: the replica's misfit + gradient, 8 solves)."""
     if rank != 0:
         return None
-    from oracle import discretize as D
-    from oracle import fwi
-    prob, desc, vref = workload(args.workload, 0)
-    pml_o = D.PmlParams(v_ref=vref)
-    d = fwi.forward_data(prob, pml_o, prob.m_true)
+    prob, _, desc, vref, _ = workload(args.workload, 0, size)
+    cores, model = host_info()
     steps = []
-    total = args.warmup + args.steps
-    for i in range(total):
-        dt, n = oracle_step(prob, d, i % len(prob.freqs), pml_o)
-        if i >= args.warmup:
-            steps.append((dt, n))
+    if args.workload == "cfg4":
+        sample = f"oracle misfit+gradient of the {REPLICA_DESC}, LU, 1 thread"
+        for i in range(args.warmup + args.steps):
+            dt, n, _ = oracle_replica_step()
+            if i >= args.warmup:
+                steps.append((dt, n))
+    else:
+        from oracle import discretize as D
+        from oracle import fwi
+        pml_o = D.PmlParams(v_ref=vref)
+        d = fwi.forward_data(prob, pml_o, prob.m_true)
+        sample = "oracle misfit+gradient, one frequency x all shots per step (SuperLU, 1 thread)"
+        for i in range(args.warmup + args.steps):
+            fi = i % len(prob.freqs)
+            p1 = prob.with_(freqs=(prob.freqs[fi],))
+            t0 = time.perf_counter()
+            fwi.misfit_grad(p1, pml_o, d[fi:fi + 1])
+            if i >= args.warmup:
+                steps.append((time.perf_counter() - t0, 2 * len(prob.src)))
     t = sum(s[0] for s in steps)
     n = sum(s[1] for s in steps)
     value = n / t
@@ -347,10 +509,9 @@ def run_reference(args, rank, size):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (seeded generators, synth/)",
-        "config": {"workload": desc + " — each step one frequency (100 solves) of it",
-                   "solves_per_step_per_gpu": 2 * len(prob.src)},
+        "config": {"workload": desc + " — the oracle's step: " + sample, "solves_per_step_per_gpu": n // args.steps},
         "cpu_baseline": {"value": round(value, 4), "unit": "solves/s", "cores": 1, "kind": "oracle",
-                         "sample": "oracle misfit+gradient, one frequency x 50 shots per step (SuperLU, 1 thread)"},
+                         "sample": sample, "host": {"nproc": cores, "lscpu_model": model}},
         "e2e": {"value": round(value, 4), "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -363,11 +524,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
-    ap.add_argument("--workload", default="cfg2")
-    ap.add_argument("--max-rhs", type=int, default=0, help="RHS per joint batch (0 = all pairs)")
+    ap.add_argument("--workload", default="cfg4", choices=["cfg4", "cfg2", "cfg3"])
+    ap.add_argument("--max-rhs", type=int, default=0, help="RHS per joint batch (0 = the workload's default)")
     ap.add_argument("--probe-stride", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-matvec", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary cfg2 / c64 legs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -386,15 +548,27 @@ def main():
     torch.cuda.set_device(local)
     if size > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    out, prob = run_ours(args, rank, size, local)
+    out, res = run_ours(args, rank, size, local)
+    if size == 1 and not args.no_extra:
+        # secondary legs (not `value`): the other dtype of the headline workload, and cfg2
+        from paper_1703_09268_b200 import api
+        other = api.C64 if args.dtype == "c128" else api.C128
+        r2 = evaluate_workload(args.workload, args, rank, size, other, 2, 1, profile=False, e2e=False, clocks=False)
+        out["other_dtype"] = {"dtype": "c64 (mixed: c128 outer FGMRES)" if other == api.C64 else "c128",
+                              "value": round(r2["value"], 4), "unit": "solves/s", "steps": 2,
+                              "ms_per_step": round(r2["ms"] / 2, 1)}
+        if args.workload != "cfg2":
+            a2 = argparse.Namespace(**vars(args))
+            a2.max_rhs = 0
+            r3 = evaluate_workload("cfg2", a2, rank, size, api.C128, 3, 2, profile=False, e2e=False, clocks=False)
+            out["cfg2"] = {"workload": r3["desc"], "dtype": "c128", "value": round(r3["value"], 3), "unit": "solves/s",
+                           "steps": 3, "ms_per_step": round(r3["ms"] / 3, 1)}
     if rank == 0:
         if size == 1 and not args.no_matvec:
-            out["matvec"] = {k: matvec_probe(*k_) for k, k_ in
-                             (("c128_b1_256", ("c128", 256, 1)), ("c128_b1_512", ("c128", 512, 1)),
-                              ("c128_b4_256", ("c128", 256, 4)), ("c64_b4_256", ("c64", 256, 4)))}
+            out["matvec"] = matvec_sweep()
         if size == 1 and not args.no_cpu_baseline:
-            from oracle import discretize as D
-            out["cpu_baseline"] = cpu_baseline(prob, D.PmlParams(v_ref=3000.0))
+            per_solve = out["solve_roofline"]["alg_bytes_per_step"] / out["config"]["solves_per_step_per_gpu"]
+            out["cpu_baseline"] = cpu_baseline_cfg4(per_solve) if args.workload == "cfg4" else None
         print(json.dumps(out), flush=True)
     if size > 1:
         dist.barrier()

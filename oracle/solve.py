@@ -29,11 +29,20 @@ class LU:
             return self.lu.solve(Q, trans="H" if adjoint else "N")
 
 
+class NotConverged(RuntimeError):
+    pass
+
+
 def gmres_solve(H: sp.spmatrix, q: np.ndarray, rtol: float = 1e-10, restart: int = 100,
                 adjoint: bool = False, maxiter: int = 200) -> np.ndarray:
-    """Unpreconditioned restarted GMRES(restart), x0 = 0, to ||q - Hx|| <= rtol ||q||."""
+    """c.2 step 3 "otherwise": unpreconditioned restarted GMRES(restart) [72], x0 = 0,
+    to ||q - Hx|| <= rtol ||q|| (D9); H^H for adjoints (D6 via the explicit transpose).
+    Raises NotConverged when scipy reports info != 0 or the TRUE residual misses rtol."""
     A = H.conj().T.tocsr() if adjoint else H
     x, info = spla.gmres(A, q, rtol=rtol, atol=0.0, restart=restart, maxiter=maxiter)
+    res = float(np.linalg.norm(q - A @ x) / np.linalg.norm(q))
+    if info != 0 or not res <= rtol * (1 + 1e-6):
+        raise NotConverged(f"GMRES({restart}) did not reach rtol {rtol:g}: info {info}, true residual {res:.3e}")
     return x
 
 

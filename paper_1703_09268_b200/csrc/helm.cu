@@ -14,6 +14,8 @@
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <type_traits>
 #include <string>
 #include <vector>
@@ -168,6 +170,7 @@ struct helm_op {
   helm_pml pml{};
   helm_mlopts ml{};
   helm_dtype dtype = HELM_C128;
+  int device = 0;              // CUDA device the op's memory lives on
   int max_rhs = 1;
   double omega = 0.0;          // = omegas[0]
   int nop = 1;                 // operators (frequencies) sharing the geometry (joint batches)
@@ -285,6 +288,33 @@ template <int N = 1, typename F> void dispatch_k(int k, F&& f) {
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;
+}
+
+// Opt-in dynamic shared memory: the limit is ONE setting per (kernel, device) shared by every
+// host thread, so it is raised once per (kernel instantiation, device) to the device's
+// opt-in maximum (227 KB on B200) and never lowered — no thread can shrink a limit another
+// thread's launch relies on. Cheap after the first call (a set lookup).
+std::mutex g_optin_mu;
+std::set<std::pair<const void*, int>> g_optin_done;   // (kernel, device)
+template <typename K> void ensure_smem_optin(K kern) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const std::pair<const void*, int> key{reinterpret_cast<const void*>(kern), dev};
+  std::lock_guard<std::mutex> lk(g_optin_mu);
+  if (g_optin_done.count(key)) return;
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  g_optin_done.insert(key);
+}
+int smem_optin() {
+  static const int v = [] {
+    int dev = 0, o = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&o, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return o;
+  }();
+  return v;
 }
 
 // Hot-path launches use programmatic dependent launch (see common.cuh pdl_wait): the
@@ -446,16 +476,26 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
     c.S = t.s_fixed >= 4 ? std::min(t.s_fixed, 12) : (int)std::min<size_t>(12, (220 * 1024) / (t.occ_target * sb));
     c.S = std::max(c.S, 4);
     c.smem = c.S * sb + 8 * c.S;   // ring + one mbarrier per stage (TMA)
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem));
+    ensure_smem_optin(kern);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ, kern, NT, c.smem));
     if (c.occ < 1) throw HelmErr{HELM_ERR_STATE, "plane kernel does not fit on an SM"};
     return c;
   }();
+  ensure_smem_optin(kern);   // this device (the cached configuration may come from another one)
   const PlaneSplit sp = plane_split(groups, (long long)num_sms() * cfg.occ, a.ntx * a.nty, a.g.nz);
   a.cpg = sp.cpg; a.nzc = sp.nzc; a.zlen = sp.zlen;
   a.S = cfg.S;
   const long long cpg = sp.cpg;
   pdl_launch(kern, dim3((unsigned)(groups * cpg)), dim3(NT), cfg.smem, st, a);
+}
+
+// Largest number of operators (frequencies) one 2D joint batch may hold: the march kernel
+// keeps 3 z coefficients per plane and operator in shared memory next to a ring of at least
+// 3 stages of its widest mode (the last fused GMRES step, HELM_KMAX basis tiles).
+template <typename R> int march_max_ops(int nz) {
+  const long long ring = 4LL * 3 * MarchShape<R, 4, HELM_KMAX - 1>::stage_bytes;
+  const long long per_op = 3LL * nz * sizeof(cx<R>);
+  return (int)std::max(0LL, std::min<long long>(HELM_MAXOP, (smem_optin() - ring - 16) / per_op));
 }
 
 // 2D: register z-march kernel (march2d.cuh), one warp per (RHS, 30-point strip, z-chunk)
@@ -475,13 +515,14 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
   int S = s_fix >= 3 ? s_fix : (int)(((220 * 1024) / occ_t - (long long)zbytes) / (4 * SB));
   S = std::max(3, std::min(S, 16));
   const size_t smem = zbytes + (size_t)4 * S * SB;
+  // the z table of every operator of the batch lives in shared memory (fwi_run closes joint
+  // batches before this limit, march_max_ops); a grid too deep for even one operator fails here
+  REQ(smem <= (size_t)smem_optin(), HELM_ERR_SHAPE,
+      "2D grid too deep for the march kernel: nz_ext x operators = " + std::to_string(a.g.nz * a.g.nop) +
+          " z-table entries exceed shared memory");
   struct Cfg { size_t smem = 0; int occ = 0; };
   thread_local Cfg cache[4];   // small per-thread cache of (smem -> occupancy)
-  thread_local size_t attr_max = 48 * 1024;   // the opt-in limit only ever grows
-  if (smem > attr_max) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_max = smem;
-  }
+  ensure_smem_optin(kern);
   int occ = 0;
   for (auto& c : cache)
     if (c.smem == smem) { occ = c.occ; break; }
@@ -912,6 +953,14 @@ void validate_grid(const helm_grid* g) {
   for (int a = 0; a < 3; ++a) REQ(g->n[a] + g->pml[a][0] + g->pml[a][1] < (1LL << 30), HELM_ERR_SHAPE, "axis too large");
 }
 
+// Model and PML checks of helm_setup, also applied when a cached fwi op is reused.
+void validate_model_pml(const helm_grid& g, const double* m, const helm_pml& P) {
+  REQ(std::isfinite(P.R) && P.R > 0 && P.R < 1 && P.power >= 0 && std::isfinite(P.v_ref), HELM_ERR_ARG,
+      "bad PML parameters");
+  const size_t n_int = (size_t)g.n[0] * g.n[1] * g.n[2];
+  for (size_t i = 0; i < n_int; ++i) REQ(m[i] > 0 && std::isfinite(m[i]), HELM_ERR_ARG, "m must be > 0 and finite");
+}
+
 void op_set_model(helm_op* op, const double* m_host) {
   op->clear_graphs();
   const helm_grid& G = op->grid;
@@ -951,9 +1000,8 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
   REQ(o.ks_i <= HELM_KMAX && o.kc_i <= HELM_KMAX && k_inner <= HELM_KMAX && k_inner >= 1, HELM_ERR_ARG,
       "inner Krylov dimension exceeds HELM_KMAX");
   helm_pml P = pml ? *pml : helm_pml{1e-4, 2, 0.0};
-  REQ(P.R > 0 && P.R < 1 && P.power >= 0, HELM_ERR_ARG, "bad PML parameters");
+  validate_model_pml(*grid, m, P);
   const size_t n_int = (size_t)grid->n[0] * grid->n[1] * grid->n[2];
-  for (size_t i = 0; i < n_int; ++i) REQ(m[i] > 0 && std::isfinite(m[i]), HELM_ERR_ARG, "m must be > 0 and finite");
   double vref = P.v_ref;
   if (!(vref > 0)) {
     double mmin = m[0];
@@ -967,6 +1015,7 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
   REQ(major == 10 && minor == 0, HELM_ERR_STATE, "libhelm is built for sm_100a (B200) only");
 
   std::unique_ptr<helm_op> op(new helm_op());
+  op->device = dev;
   op->grid = *grid; op->pml = P; op->ml = o; op->dtype = dtype; op->max_rhs = max_rhs; op->omega = omega;
   op->vref = vref; op->st = st; op->dim = grid->ndim; op->k_inner = k_inner;
   // hierarchy sizes (D13): N -> ceil(N/2) on active axes, stop when an axis would be < 5
@@ -983,6 +1032,17 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
   }
   if (L < o.levels) g_err = "warning: grid too small for the requested depth; using " + std::to_string(L) + " levels";
   op->L = L;
+  {   // fewer than 4 points per wavelength on the finest grid is a warning, not a
+      // failure (readable via helm_last_error); depth is limited by ppw on coarse grids
+    double mmax = m[0];
+    for (size_t i = 1; i < n_int; ++i) mmax = std::max(mmax, m[i]);
+    const double ppw = 2.0 * M_PI / (omega * std::sqrt(mmax)) / grid->h;
+    if (ppw < 4.0) {
+      char buf[160];
+      std::snprintf(buf, sizeof buf, "warning: grid too coarse: %.2f points per wavelength at v_min (< 4)", ppw);
+      g_err = g_err.empty() ? std::string(buf) : g_err + "; " + buf;
+    }
+  }
   for (int l = 0; l < L; ++l) {
     LevelDev& Lv = op->lev[l];
     Lv.nx = dims[l][0]; Lv.ny = dims[l][1]; Lv.nz = dims[l][2];
@@ -1496,8 +1556,22 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
     for (int b = 0; b < nb; ++b)
       std::memcpy(d_out + 2 * (((size_t)fi_h[b] * ns + si_h[b]) * nrec), &dbat[(size_t)b * nrec], sizeof(double2) * nrec);
   };
-  for (p0 = 0; p0 < npairs; p0 += B) {
-    const int nb = (int)std::min<long long>(B, npairs - p0);
+  // operators one joint batch may hold: HELM_MAXOP, and in 2D what the march kernel's
+  // shared-memory z table takes (deep 2D grids x many frequencies)
+  const int max_ops = op->dim == 2 ? march_max_ops<R>(op->lev[0].nz) : HELM_MAXOP;
+  REQ(max_ops >= 1, HELM_ERR_SHAPE, "2D grid too deep for the march kernel (nz_ext = " +
+                                        std::to_string(op->lev[0].nz) + ")");
+  int nb = 0;
+  for (p0 = 0; p0 < npairs; p0 += nb) {
+    // the batch: up to B pairs in order, closed early before a (max_ops + 1)-th frequency
+    nb = 0;
+    for (int nf = 0, lf = -1; nb < B && p0 + nb < npairs; ++nb) {
+      if (pf[p0 + nb] != lf) {
+        if (nf == max_ops) break;
+        ++nf;
+        lf = pf[p0 + nb];
+      }
+    }
     // the batch's operators (distinct frequencies, in order) and per-RHS data
     wop.clear();
     int last_f = -1;
@@ -1510,7 +1584,7 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
       w2_h[b] = wop.back() * wop.back();
       srcb_h[b] = offg ? si : sext[si];
     }
-    REQ((int)wop.size() <= HELM_MAXOP, HELM_ERR_ARG, "more than HELM_MAXOP frequencies in one batch");
+    REQ((int)wop.size() <= max_ops, HELM_ERR_STATE, "joint batch holds too many operators");
     op_set_omegas(op, wop.data(), (int)wop.size());
     op_set_rop(op, rop_h);
     CK(cudaMemcpyAsync(amp_d, amp_h.data(), sizeof(double2) * nb, cudaMemcpyHostToDevice, st));
@@ -1605,7 +1679,10 @@ helm_op* fwi_op(const helm_grid* grid, const double* m, double omega, const helm
       if (a.n[i] != b.n[i] || a.pml[i][0] != b.pml[i][0] || a.pml[i][1] != b.pml[i][1]) return false;
     return true;
   };
-  if (o && o->dtype == dtype && o->max_rhs == max_rhs && same(o->grid, *grid)) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (o && o->device == dev && o->dtype == dtype && o->max_rhs == max_rhs && same(o->grid, *grid)) {
+    validate_model_pml(*grid, m, *pml);
     o->st = st;
     o->pml = *pml;
     o->vref = pml->v_ref;

@@ -1,4 +1,4 @@
-"""BASELINE configs[3] at full size on one GPU: 3D layered model 200^3 + PML 10 (220^3
+"""BASELINE configs[3] at full size on one GPU: 3D layered model 200^3 + PML 20 (240^3
 extended), h = 25 m, f = 6 Hz, 64 surface sources, 40,000 receivers. Generates d_obs at the
 true model (FORW_MODEL, rtol 1e-8), then times one misfit + gradient evaluation (128 solves,
 rtol 1e-6) and prints solves/s, outer cycles, the library's algorithmic bytes and the
@@ -55,7 +55,7 @@ api.profile(False, 1)
 fgh = fg.cpu().numpy()
 nsolve = len(rep)
 byts = sum(r["bytes_alg"] for r in rep)
-out = {"workload": f"cfg4 {a.n}^3 + PML 10, 64 sources, 6 Hz, {a.dtype}, max_rhs {a.max_rhs}",
+out = {"workload": f"cfg4 {a.n}^3 + PML {p.pml[0][0]}, 64 sources, 6 Hz, {a.dtype}, max_rhs {a.max_rhs}",
        "gen_s": round(tg, 1), "forward_data_s": round(tf, 1), "eval_s": round(ms / 1e3, 2),
        "solves": nsolve, "solves_per_s": round(nsolve / (ms / 1e3), 3),
        "cycles": {"min": min(r["outer_cycles"] for r in rep), "max": max(r["outer_cycles"] for r in rep),

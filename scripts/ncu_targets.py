@@ -47,9 +47,12 @@ elif what == "probe":
         p, f, vref, nrhs = synth.cfg2(freqs=(5.0,)), 5.0, 3000.0, 50
     elif case == "cfg2_150":
         p, f, vref, nrhs = synth.cfg2(freqs=(5.0,)), 5.0, 3000.0, 150
+    elif case.startswith("cfg4_"):   # cfg4 full size, nrhs = the suffix (bench: 8)
+        p, f, vref, nrhs = synth.cfg4(), 6.0, 4500.0, int(case.split("_")[1])
     else:
         p, f, vref, nrhs = synth.cfg5(256), 6.0, 4500.0, 1
-    op = api.helm_setup(api.Grid.of(p), p.m, 2 * np.pi * f, api.Pml(v_ref=vref), api.C128, max_rhs=nrhs)
-    print(api.probe_kernel(op, level, kind, nv, nrhs, reps=4))
+    dt = api.C64 if os.environ.get("PROBE_DTYPE") == "c64" else api.C128
+    op = api.helm_setup(api.Grid.of(p), p.m, 2 * np.pi * f, api.Pml(v_ref=vref), dt, max_rhs=nrhs)
+    print(api.probe_kernel(op, level, kind, nv, nrhs, reps=int(os.environ.get("PROBE_REPS", "4"))))
     torch.cuda.synchronize()
 print("ok")

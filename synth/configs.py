@@ -50,8 +50,13 @@ class Problem:
 
 
 def node_id(ix, iy, iz, n) -> np.ndarray:
-    nx, ny, _ = n
-    return np.asarray(ix, np.int64) + nx * (np.asarray(iy, np.int64) + ny * np.asarray(iz, np.int64))
+    """Linear interior node id; every axis index must lie inside the interior (no wrap-around)."""
+    nx, ny, nz = n
+    ix, iy, iz = (np.asarray(v, np.int64) for v in (ix, iy, iz))
+    for v, m, a in ((ix, nx, "x"), (iy, ny, "y"), (iz, nz, "z")):
+        if v.size and (v.min() < 0 or v.max() >= m):
+            raise ValueError(f"node index out of the interior along {a}: [{v.min()}, {v.max()}] vs n = {m}")
+    return ix + nx * (iy + ny * iz)
 
 
 def random_complex(shape, seed: int = 1, dtype=np.complex128) -> np.ndarray:
@@ -153,8 +158,12 @@ def layered_model(n: int, seed: int = 0, noise: float = 0.05):
     return v0, v0 * (1.0 + nz)
 
 
-def cfg4(n: int = 200, h: float = 25.0, pml: int = 10, nsrc_side: int = 8,
+def cfg4(n: int = 200, h: float = 25.0, pml: int = 20, nsrc_side: int = 8,
          src_pitch: int = 25, src_off: int = 12, f: float = 6.0, name="cfg4") -> Problem:
+    """Layered 3D FWI problem (BASELINE configs[3]). PML width (R9, revised in round 2): 20
+    points = one wavelength at the model's mean layer velocity (3000 m/s at 6 Hz, h = 25 m);
+    10 points (one wavelength at v_min) is only 1/3 wavelength in the fast bottom layers and
+    measured 13 / 17 forward / adjoint outer cycles against 5 / 5 at 20."""
     v0, vt = layered_model(n)
     N = (n, n, n)
     k = src_off + src_pitch * np.arange(nsrc_side)
@@ -167,8 +176,9 @@ def cfg4(n: int = 200, h: float = 25.0, pml: int = 10, nsrc_side: int = 8,
 
 
 def cfg4_replica(n: int = 24, pml: int = 6) -> Problem:
-    """Parity replica of cfg4 from the same generator: 4 sources at {6,18}^2, n^2 receivers."""
-    return cfg4(n=n, pml=pml, nsrc_side=2, src_pitch=12, src_off=6, name=f"cfg4r{n}")
+    """Parity replica of cfg4 from the same generator: 4 sources at {n/4, 3n/4}^2 (n = 24:
+    {6, 18}^2), n^2 receivers."""
+    return cfg4(n=n, pml=pml, nsrc_side=2, src_pitch=n // 2, src_off=n // 4, name=f"cfg4r{n}")
 
 
 def cfg5(N: int) -> Problem:

@@ -7,7 +7,7 @@
   oracle's own assembled H (<= 1e-6), analytic -e^{ikr}/(4 pi r) within 15 % (STD2 at 12.5
   points per wavelength, SURVEY c.4), and the 8-source batch.
 * cfg4 (configs[3]) replica at 24^3 from the same generator: f, g vs oracle LU; and at full
-  size (220^3 extended) one solve whose residual, recomputed by the oracle's rows of H on
+  size (240^3 extended) one solve whose residual, recomputed by the oracle's rows of H on
   sampled z-slabs, is bounded by the certified 1e-6.
 * cfg5 (configs[4]) 256^3 matvec, c128 and c64, batch 4, forward and adjoint: sampled
   z-slabs vs the oracle's slab rows of H (c128 <= 1e-12, c64 <= 1e-5).
@@ -150,7 +150,7 @@ def test_table3_smallest_cell_certified():
 
 
 def test_cfg4_fullsize_solve_sampled_residual():
-    """cfg4 (configs[3]) at full size (200^3 + PML 10, 6 Hz, c128, bench-like preconditioned
+    """cfg4 (configs[3]) at full size (200^3 + PML 20, 6 Hz, c128, bench-like preconditioned
     solve): the residual q - H u recomputed by the oracle's own rows of H on sampled z-slabs
     (the source slab, PML slabs and random interior ones) is bounded by the solver's certified
     global residual: sqrt(sum_slabs ||r_slab||^2) <= ||r|| <= 1e-6 ||q||."""

@@ -29,6 +29,20 @@ def test_taylor_first_and_second_order():
     assert np.all(np.abs(s1 - 2) < 0.25), s1         # O(h^2) (P:318 line 2)
 
 
+def test_taylor_3d():
+    """The paper's Taylor test is 3D (§6.1): the oracle's f, g on tiny3d (LU fields)
+    give e0 slope 1 and e1 slope 2."""
+    p = synth.tiny3d()
+    pml = D.PmlParams(v_ref=3000.0)
+    d = fwi.forward_data(p, pml, p.m_true)
+    _, g = fwi.misfit_grad(p, pml, d)
+    dm = p.m_true - p.m
+    ts = 2.0 ** -np.arange(2, 9)
+    e0, e1 = fwi.taylor_errors(lambda m: fwi.misfit_grad(p, pml, d, m)[0], p.m, dm, g, ts)
+    assert np.all(np.abs(_slopes(e0, ts) - 1) < 0.25), _slopes(e0, ts)
+    assert np.all(np.abs(_slopes(e1, ts) - 2) < 0.25), _slopes(e1, ts)
+
+
 def test_interior_only_gradient_fails_taylor():
     """R11: restricting Re(w^2 conj(u) v) to the interior (instead of E^T) loses second order."""
     p, pml, d = _setup()
