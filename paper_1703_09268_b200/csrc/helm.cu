@@ -439,7 +439,7 @@ template <typename R> const cx<R>* level_zq(const LevelDev& L, int adj);
 template <> const double2* level_zq<double>(const LevelDev& L, int adj) { return L.zq64[adj]; }
 template <> const float2* level_zq<float>(const LevelDev& L, int adj) { return L.zq32[adj]; }
 
-struct PlaneCfg { int S = 0, occ = 0; size_t smem = 0; };
+struct PlaneCfg { int S = 0, occ = 0, nf = 0; size_t smem = 0; };
 
 // Split of a group's T tiles x nz planes over its CTAs (one resident wave of G CTAs over
 // all groups): the z-chunk count minimising waves x (chunk planes + 2 halo planes).
@@ -460,7 +460,7 @@ PlaneSplit plane_split(int groups, long long G, int T, int nz) {
 }
 
 // Launch with exactly one resident wave (groups x cpg CTAs, see stencil.cuh).
-template <typename R, int MODE, int NV, bool YC, int PY = plane_py<MODE, YC>()>
+template <typename R, int MODE, int NV, bool YC, int PY = plane_py<MODE, YC>(), bool SPLIT = false>
 void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
   if constexpr (MODE == 0 && PY == 4) {   // HELM_PLANE_PY=2: two rows per thread (A/B)
     static const bool py2 = env_int("HELM_PLANE_PY", 4) == 2;
@@ -468,23 +468,47 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
   }
   using Sh = PlaneShape<MODE, NV>;
   constexpr int NT = 32 * 8 / PY;
-  constexpr size_t sb = PlaneSmem<R, 32, 8, Sh::NX, Sh::NP, YC>::stage_bytes;
-  auto kern = k_plane<R, 32, 8, PY, MODE, NV, YC>;
+  constexpr size_t sb = PlaneSmem<R, 32, 8, Sh::NX, Sh::NP, YC, SPLIT>::stage_bytes;
+  auto kern = k_plane<R, 32, 8, PY, MODE, NV, YC, SPLIT>;
   static const PlaneCfg cfg = [&] {
     PlaneCfg c;
     const PlaneTune& t = plane_tune<R, PY>();
-    c.S = t.s_fixed >= 4 ? std::min(t.s_fixed, 12) : (int)std::min<size_t>(12, (220 * 1024) / (t.occ_target * sb));
-    c.S = std::max(c.S, 4);
-    c.smem = c.S * sb + 8 * c.S;   // ring + one mbarrier per stage (TMA)
+    if constexpr (SPLIT) {
+      // split-ring fused steps: D raw stages + nf formed slots per CTA at `occ` CTAs per SM
+      // (default 2 complex128 / 3 complex64; HELM_SPLIT_OCC, HELM_SPLIT_D override)
+      const size_t fb = FormSlot<R, 32, 8, YC>::bytes;
+      const int occ_t = std::max(1, env_int("HELM_SPLIT_OCC", sizeof(R) == 8 ? 2 : 3));
+      const long long budget = (long long)(smem_optin() - 1024) / occ_t;
+      c.nf = 4;
+      long long d = (budget - 4 * (long long)fb) / (long long)(sb + 8);
+      if (d < 2) { c.nf = 3; d = (budget - 3 * (long long)fb) / (long long)(sb + 8); }
+      const int dfix = env_int("HELM_SPLIT_D", 0);
+      c.S = dfix >= 2 ? dfix : (int)std::max(2LL, std::min(12LL, d));
+      c.smem = c.S * sb + c.nf * fb + 8 * c.S;
+    } else {
+      c.S = t.s_fixed >= 4 ? std::min(t.s_fixed, 12) : (int)std::min<size_t>(12, (220 * 1024) / (t.occ_target * sb));
+      c.S = std::max(c.S, 4);
+      c.smem = c.S * sb + 8 * c.S;   // ring + one mbarrier per stage (TMA)
+    }
     ensure_smem_optin(kern);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ, kern, NT, c.smem));
     if (c.occ < 1) throw HelmErr{HELM_ERR_STATE, "plane kernel does not fit on an SM"};
+    if (env_int("HELM_DEBUG", 0)) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kern);
+      std::fprintf(stderr, "[helm] plane R=%zu mode=%d nv=%d py=%d split=%d S=%d nf=%d smem=%zu regs=%d occ=%d\n", sizeof(R),
+                   MODE, NV, PY, (int)SPLIT, c.S, c.nf, c.smem, fa.numRegs, c.occ);
+    }
     return c;
   }();
   ensure_smem_optin(kern);   // this device (the cached configuration may come from another one)
   const PlaneSplit sp = plane_split(groups, (long long)num_sms() * cfg.occ, a.ntx * a.nty, a.g.nz);
   a.cpg = sp.cpg; a.nzc = sp.nzc; a.zlen = sp.zlen;
   a.S = cfg.S;
+  a.nf = cfg.nf;
+  if (env_int("HELM_DEBUG", 0) > 1)
+    std::fprintf(stderr, "[helm] plane launch mode=%d nv=%d split=%d groups=%d cpg=%d nzc=%d zlen=%d tiles=%d\n", MODE, NV,
+                 (int)SPLIT, groups, sp.cpg, sp.nzc, sp.zlen, a.ntx * a.nty);
   const long long cpg = sp.cpg;
   pdl_launch(kern, dim3((unsigned)(groups * cpg)), dim3(NT), cfg.smem, st, a);
 }
@@ -633,8 +657,29 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
   if (mode == 0) run_plane<R, 0, 0, true>(a, groups, units, op->st);
   else if (mode == 1) run_plane<R, 1, 0, true>(a, groups, units, op->st);
   else if (mode == 2) dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, true>(a, groups, units, op->st); });
-  else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_plane<R, 3, decltype(c)::value, true>(a, groups, units, op->st); });
-  else dispatch_k0(nv, [&](auto c) { run_plane<R, 4, decltype(c)::value, true>(a, groups, units, op->st); });
+  else {
+    // fused steps that form v_nv (nv > 0): split raw / formed rings (stencil.cuh FormSlot) when
+    // every operand comes by TMA. Same-box A/B (profiles/r02/probe_split_ab.txt): with fewer,
+    // deeper CTAs the split ring loses on steps 1-3 (the per-plane wait/form/compute chain of a
+    // CTA is the limit, not bytes in flight) and wins on the last complex128 step (NV = 4:
+    // +8 % at level 0, +7 % at level 1). HELM_SPLIT: 0 off, 1 (default) that step only, 2 all.
+    static const int split_mode = env_int("HELM_SPLIT", 1);
+    const bool split = a.tma && a.tmq && nv > 0 &&
+                       (split_mode == 2 || (split_mode == 1 && sizeof(R) == 8 && mode == 4 && nv >= 4));
+    auto go = [&](auto c) {
+      constexpr int NVc = decltype(c)::value;
+      if constexpr (NVc > 0) {
+        if (split) {
+          if (mode == 3) run_plane<R, 3, NVc, true, plane_py<3, true>(), true>(a, groups, units, op->st);
+          else run_plane<R, 4, NVc, true, plane_py<4, true>(), true>(a, groups, units, op->st);
+          return;
+        }
+      }
+      if (mode == 3) run_plane<R, 3, NVc, true>(a, groups, units, op->st);
+      else run_plane<R, 4, NVc, true>(a, groups, units, op->st);
+    };
+    dispatch_k0(nv, go);
+  }
   CKL();
   prof_end(cls, op->st, acct(op, l, per * a.g.N, true, nrhs));
 }

@@ -110,7 +110,8 @@ template <typename R> struct PlaneArgs {
   int nrhs, ntx, nty;      // row tiles: ntx x nty per group (nty = 1 in 2D)
   int cpg;                 // CTAs per group
   int nzc, zlen;           // z-chunks per tile and their length
-  int S;                   // ring stages (>= 4)
+  int S;                   // ring stages (>= 4; split-ring fused steps: raw stages D >= 2)
+  int nf;                  // split-ring fused steps: formed slots (3: two barriers per plane, 4: one)
   int tma;                 // TMA stages (tm[0] = x / W, tm[1 + i] = V_i halo'd tiles; tmm = m, tmz = z
                            // coefficients) instead of per-thread cp.async
   CUtensorMap tm[HELM_KMAX + 1];
@@ -120,7 +121,7 @@ template <typename R> struct PlaneArgs {
   RedBuf rb;
 };
 
-template <typename R, int BX, int BY, int NX, int NP, bool YC>
+template <typename R, int BX, int BY, int NX, int NP, bool YC, bool MREG = false>
 struct PlaneSmem {
   static constexpr int YH = YC ? 1 : 0;              // y-halo rows (3D only)
   // TMA boxes must start 16-B aligned along x (measured on B200: an unaligned start faults
@@ -136,12 +137,27 @@ struct PlaneSmem {
   // m is staged in the ring, except for the complex128 five-tile stages (the last Arnoldi
   // steps), where it is register-prefetched two planes ahead so that the stage fits two
   // CTAs per SM (measured: 3.3 -> 4.1 TB/s there; smaller stages are faster with m staged)
-  static constexpr bool MR = sizeof(cx<R>) != 16 || NX < 5;
+  // (MREG: m always register-prefetched — the split-ring fused steps below)
+  static constexpr bool MR = !MREG && (sizeof(cx<R>) != 16 || NX < 5);
   static constexpr size_t m_off = (size_t)NX * XS * sizeof(cx<R>);
   static constexpr size_t p_off = m_off + (MR ? PE * sizeof(R) : 0);
   static constexpr size_t z_off = p_off + (size_t)NP * PE * sizeof(cx<R>);
   static constexpr int ZR = YC ? 1 : BY;               // z-coefficient rows (2D: one per warp)
   static constexpr size_t stage_bytes = (z_off + ZR * 4 * sizeof(cx<R>) + 127) / 128 * 128;
+};
+
+// Split-ring fused Arnoldi steps (MODE 3/4, NV > 0, TMA fills): the raw operands of a plane
+// (halo'd tiles of W and V_0..V_{NV-1}) live in a D-stage TMA ring only until v_NV is formed
+// from them; the formed halo'd tile (and the plane's z coefficients) go to one of NF = 4
+// small "formed" slots that the stencil reads for planes z-1, z, z+1, and each thread keeps
+// the own points of V_0..V_{NV-1} (the projection operands of plane z) in registers. A raw
+// stage is refilled right after its plane is formed, so D-1 planes stay in flight instead of
+// S-3 with full-size stages (the ncu capture of the old design: 1 plane in flight per CTA,
+// 12 warps/SM, DRAM 44-51 % busy at level 1), and one CTA barrier per plane suffices.
+template <typename R, int BX, int BY, bool YC> struct FormSlot {
+  using SM1 = PlaneSmem<R, BX, BY, 1, 0, YC, true>;
+  static constexpr size_t z_off = (size_t)SM1::XS * sizeof(cx<R>);
+  static constexpr size_t bytes = (z_off + 4 * sizeof(cx<R>) + 127) / 128 * 128;
 };
 
 // MODE 4 = MODE 3 for the LAST step of a cycle: Y = H V_NV is not stored, and ||Y||^2 is
@@ -254,7 +270,7 @@ __device__ inline void plane_epilogue(const KCtx& ctx, int r, int jstep, const d
   }
 }
 
-template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC>
+template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC, bool SPLIT = false>
 __global__ void __launch_bounds__(BX * BY / PY)
 k_plane(const __grid_constant__ PlaneArgs<R> a) {
   pdl_wait();
@@ -262,7 +278,9 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
   using C = cx<R>;
   using Sh = PlaneShape<MODE, NV>;
   constexpr int NX = Sh::NX, NP = Sh::NP, NVR = Sh::NVR;
-  using SM = PlaneSmem<R, BX, BY, NX, NP, YC>;
+  using SM = PlaneSmem<R, BX, BY, NX, NP, YC, SPLIT>;
+  using FS = FormSlot<R, BX, BY, YC>;
+  static_assert(!SPLIT || (MODE >= 3 && NV > 0 && YC), "split ring: fused GMRES steps that form v_NV (3D)");
   constexpr int YH = SM::YH;
   constexpr int NT = BX * BY / PY;
   constexpr int RS = BY / PY;          // row stride between a thread's rows
@@ -313,7 +331,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
 
   const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);
   // TMA: one mbarrier per ring stage, after the stages (stage addresses stay 128-B aligned)
-  const unsigned mbase = sbase + (unsigned)(S * SM::stage_bytes);
+  const unsigned mbase = sbase + (unsigned)(S * SM::stage_bytes + (SPLIT ? a.nf * FS::bytes : 0));
   const bool tma = a.tma != 0;
   if (tma) {
     if (threadIdx.x == 0) {
@@ -484,11 +502,6 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
       }
     }
 
-    // ring stages are tracked incrementally (no division on the streaming path)
-    auto inc = [S](int x) { return x + 1 == S ? 0 : x + 1; };
-    int s_ld = 0;
-    for (int q = 0; q < S - 1; ++q) { load(q, s_ld); s_ld = inc(s_ld); }
-    int s_m1 = 0;             // stage of plane z-1
     // model m of this thread's points: register-prefetched two planes ahead (complex128)
     R mr0[PY], mr1[PY], mr2[PY];
     auto ldm = [&](int zz, R (&dst)[PY]) {
@@ -497,35 +510,13 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
         dst[k] = (rok[k] && zz < z1) ? __ldg(g.m + (YC ? mofs0 + (long long)k * RS * nx : mofs0) + (long long)zz * plane)
                                      : (R)0;
     };
-    if constexpr (!SM::MR) { ldm(z0, mr0); ldm(z0 + 1, mr1); }
-    for (int z = z0; z < z1; ++z) {
-      const int q = z - z0 + 1;
-      if (cpa_on) cpa_wait_n(S - 4);   // this thread's groups <= q+1 complete (committed: <= q+S-3)
-      if (tma) {                // ... and the TMA tiles of planes <= q+1 (stage s_m1 + 2)
-        const int sw = inc(inc(s_m1));
-        if (z == z0) {
-          mbar_wait(mbase + 8 * s_m1, ((pbits >> s_m1) & 1u) ^ 1u);
-          mbar_wait(mbase + 8 * inc(s_m1), ((pbits >> inc(s_m1)) & 1u) ^ 1u);
-        }
-        mbar_wait(mbase + 8 * sw, ((pbits >> sw) & 1u) ^ 1u);
-      }
-      csync<YC>();              // ... for every thread; stage (q-2)%S is free again
-      load(q + S - 2, s_ld);    // S-3 planes in flight while plane z is computed
-      s_ld = inc(s_ld);
-      const int s_0 = inc(s_m1), s_p1 = inc(s_0);
-      if constexpr (FORM) {
-        if (z == z0) { form(s_m1); form(s_0); }
-        form(s_p1);
-        csync<YC>();
-      }
-      const unsigned char* st1 = smem + s_0 * SM::stage_bytes;
-      const C* X0 = reinterpret_cast<const C*>(smem + s_m1 * SM::stage_bytes);
-      const C* X1 = reinterpret_cast<const C*>(st1);
-      const C* X2 = reinterpret_cast<const C*>(smem + s_p1 * SM::stage_bytes);
-      const R* Ms = reinterpret_cast<const R*>(st1 + SM::m_off);
-      if constexpr (!SM::MR) ldm(z + 2, mr2);
-      const C* Ps = reinterpret_cast<const C*>(st1 + SM::p_off);
-      const C* Zt = reinterpret_cast<const C*>(st1 + SM::z_off);
+    // split ring: own points of V_0..V_{NV-1} of the plane being computed (vd) and of the
+    // plane being formed (vn), captured from the raw stage before it is refilled
+    constexpr int NVD = SPLIT ? NV : 1;
+    C vd[PY][NVD], vn[PY][NVD];
+    // plane z from the tiles of planes z-1, z, z+1 (X0, X1, X2; x/y halo in X1), m (Ms or
+    // registers), the own-point operands (Ps) and the plane's z coefficients (Zt)
+    auto compute = [&](int z, const C* X0, const C* X1, const C* X2, const R* Ms, const C* Ps, const C* Zt) {
       const C lz = Zt[(YC ? 0 : ty0) * 4], dz = Zt[(YC ? 0 : ty0) * 4 + 1], uz = Zt[(YC ? 0 : ty0) * 4 + 2];
       const long long zo = (long long)z * plane;
 #pragma unroll
@@ -559,7 +550,10 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           if constexpr (LAST) ynrm += hd.x * hd.x + hd.y * hd.y;
           else *yp = hx;
 #pragma unroll
-          for (int v = 0; v < NV; ++v) acc[v] = cdot_acc(acc[v], to_d(X1[(v + 1) * SM::XS + c]), hd);
+          for (int v = 0; v < NV; ++v) {
+            if constexpr (SPLIT) acc[v] = cdot_acc(acc[v], to_d(vd[k][v]), hd);
+            else acc[v] = cdot_acc(acc[v], to_d(X1[(v + 1) * SM::XS + c]), hd);
+          }
           acc[NV] = cdot_acc(acc[NV], to_d(cur), hd);
           if constexpr (NV > 0) {
             a.vout[gofs[k] + zo] = cur;
@@ -567,10 +561,106 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           }
         }
       }
-      s_m1 = s_0;
       if constexpr (!SM::MR) {
 #pragma unroll
         for (int k = 0; k < PY; ++k) { mr0[k] = mr1[k]; mr1[k] = mr2[k]; }
+      }
+    };
+
+    if constexpr (SPLIT) {
+      // ---- split ring (TMA tiles, m in registers): raw stage of plane q is q % S, formed
+      // slot q % nf; plane q = z - z0 + 1
+      const int NF = a.nf;
+      const unsigned fb0 = (unsigned)(S * SM::stage_bytes);
+      auto fslot = [&](int q) { return smem + fb0 + (unsigned)((q % NF) * FS::bytes); };
+      auto form_split = [&](int q) {
+        const int rs = q % S;
+        const C* X = reinterpret_cast<const C*>(smem + rs * SM::stage_bytes);
+        unsigned char* fp = fslot(q);
+        C* F = reinterpret_cast<C*>(fp);
+        for (int e = threadIdx.x; e < SM::XE; e += NT) {
+          C v = cscale(X[e], cw);
+#pragma unroll
+          for (int i = 0; i < NV; ++i) v = cfma(cv[i], X[(i + 1) * SM::XS + e], v);
+          F[e] = v;
+        }
+        if (threadIdx.x < 4)
+          reinterpret_cast<C*>(fp + FS::z_off)[threadIdx.x] =
+              reinterpret_cast<const C*>(smem + rs * SM::stage_bytes + SM::z_off)[threadIdx.x];
+#pragma unroll
+        for (int k = 0; k < PY; ++k) {
+          const int c = (ty0 + k * RS + YH) * XP + tx + XO;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) vn[k][v] = X[(v + 1) * SM::XS + c];
+        }
+      };
+      auto wait_raw = [&](int q) {
+        const int rs = q % S;
+        mbar_wait(mbase + 8 * rs, ((pbits >> rs) & 1u) ^ 1u);
+      };
+      for (int q = 0; q < S; ++q) load(q, q);   // planes z0-1 .. z0+S-2 in flight
+      ldm(z0, mr0);
+      ldm(z0 + 1, mr1);
+      for (int q = 0; q < 2; ++q) {             // form planes z0-1 and z0
+        wait_raw(q);
+        form_split(q);
+        csync<YC>();
+        load(q + S, q % S);
+      }
+#pragma unroll
+      for (int k = 0; k < PY; ++k)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) vd[k][v] = vn[k][v];
+      for (int z = z0; z < z1; ++z) {
+        const int q = z - z0 + 1, qn = q + 1;
+        wait_raw(qn);
+        if (NF == 3) csync<YC>();               // compute(z-1) is done with formed slot qn % 3
+        form_split(qn);
+        csync<YC>();                            // slot qn formed; raw stage qn consumed
+        load(qn + S, qn % S);                   // S-1 planes in flight while plane z is computed
+        ldm(z + 2, mr2);
+        const unsigned char* f1 = fslot(q);
+        compute(z, reinterpret_cast<const C*>(fslot(q - 1 + NF)), reinterpret_cast<const C*>(f1),
+                reinterpret_cast<const C*>(fslot(qn)), nullptr, nullptr,
+                reinterpret_cast<const C*>(f1 + FS::z_off));
+#pragma unroll
+        for (int k = 0; k < PY; ++k)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) vd[k][v] = vn[k][v];
+      }
+    } else {
+      // ring stages are tracked incrementally (no division on the streaming path)
+      auto inc = [S](int x) { return x + 1 == S ? 0 : x + 1; };
+      int s_ld = 0;
+      for (int q = 0; q < S - 1; ++q) { load(q, s_ld); s_ld = inc(s_ld); }
+      int s_m1 = 0;             // stage of plane z-1
+      if constexpr (!SM::MR) { ldm(z0, mr0); ldm(z0 + 1, mr1); }
+      for (int z = z0; z < z1; ++z) {
+        const int q = z - z0 + 1;
+        if (cpa_on) cpa_wait_n(S - 4);   // this thread's groups <= q+1 complete (committed: <= q+S-3)
+        if (tma) {                // ... and the TMA tiles of planes <= q+1 (stage s_m1 + 2)
+          const int sw = inc(inc(s_m1));
+          if (z == z0) {
+            mbar_wait(mbase + 8 * s_m1, ((pbits >> s_m1) & 1u) ^ 1u);
+            mbar_wait(mbase + 8 * inc(s_m1), ((pbits >> inc(s_m1)) & 1u) ^ 1u);
+          }
+          mbar_wait(mbase + 8 * sw, ((pbits >> sw) & 1u) ^ 1u);
+        }
+        csync<YC>();              // ... for every thread; stage (q-2)%S is free again
+        load(q + S - 2, s_ld);    // S-3 planes in flight while plane z is computed
+        s_ld = inc(s_ld);
+        const int s_0 = inc(s_m1), s_p1 = inc(s_0);
+        if constexpr (FORM) {
+          if (z == z0) { form(s_m1); form(s_0); }
+          form(s_p1);
+          csync<YC>();
+        }
+        const unsigned char* st1 = smem + s_0 * SM::stage_bytes;
+        if constexpr (!SM::MR) ldm(z + 2, mr2);
+        compute(z, reinterpret_cast<const C*>(smem + s_m1 * SM::stage_bytes), reinterpret_cast<const C*>(st1),
+                reinterpret_cast<const C*>(smem + s_p1 * SM::stage_bytes), reinterpret_cast<const R*>(st1 + SM::m_off),
+                reinterpret_cast<const C*>(st1 + SM::p_off), reinterpret_cast<const C*>(st1 + SM::z_off));
+        s_m1 = s_0;
       }
     }
     cpa_wait<0>();

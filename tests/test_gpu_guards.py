@@ -49,13 +49,16 @@ def test_cached_fwi_op_validates_model_and_pml():
 
 def test_deep_2d_grid_splits_joint_batches():
     """nz_ext = 1000 complex128: 48 KB of z table per operator, so at most 3 operators fit next
-    to the march ring; 4 frequencies in one call are split over two batched solves."""
-    p = synth.tiny2d(nx=13, nz=990, pml=5, nsrc=2).with_(freqs=(2.0, 2.5, 3.0, 3.5))
+    to the march ring; 4 frequencies in one call are split over two batched solves. (Solved to
+    1e-10: the residual P_r u - d of this deep model's small blob is ~1e-3 of the direct wave at
+    the receivers, so solve errors are amplified ~1e3 in f and g — at 1e-8 the oracle
+    comparison measured 5e-7 / 4.7e-5 for every max_rhs, i.e. with or without the split.)"""
+    p = synth.tiny2d(nx=40, nz=960, pml=20, nsrc=2).with_(freqs=(6.0, 8.0, 10.0, 12.0))
     pml = D.PmlParams(v_ref=3000.0)
     d = fwi.forward_data(p, pml, p.m_true)
     f_ref, g_ref = fwi.misfit_grad(p, pml, d)
     fg, rep = api.fwi_misfit_grad(api.Grid.of(p), p.m, p.freqs, p.src, p.rec, d, api.Pml(v_ref=3000.0), api.C128,
-                                  api.SolveOpts(rtol=1e-8, max_outer=200), max_rhs=8)
+                                  api.SolveOpts(rtol=1e-10, max_outer=400), max_rhs=8)
     fg = fg.cpu().numpy()
     assert all(r["converged"] for r in rep)
     assert abs(fg[0] - f_ref) <= 1e-5 * f_ref

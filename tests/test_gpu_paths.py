@@ -1,7 +1,9 @@
 """GPU parity of the alternative 3D stage-fill paths, each in a fresh process (the switches are
 read once per process): per-thread cp.async instead of TMA (HELM_TMA=0), TMA tiles with m and
 the z coefficients by cp.async (HELM_TMA_MZ=0), and two rows per thread for the matvec
-(HELM_PLANE_PY=2). Each must match the assembled oracle H (c128 <= 1e-12, c64 <= 1e-5) for
+(HELM_PLANE_PY=2), the single-ring fused Arnoldi steps everywhere (HELM_SPLIT=0), the split
+ring for every fused step (HELM_SPLIT=2), also with three formed slots (two barriers per
+plane, HELM_SPLIT_OCC=4) or two raw stages (HELM_SPLIT_D=2). Each must match the assembled oracle H (c128 <= 1e-12, c64 <= 1e-5) for
 helm_apply forward / adjoint on a ragged multi-tile grid, and give a certified solve."""
 import json
 import os
@@ -47,8 +49,10 @@ print(json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("env", [{"HELM_TMA": "0"}, {"HELM_TMA_MZ": "0"}, {"HELM_PLANE_PY": "2"}],
-                         ids=["cpasync", "tma_tiles_only", "py2"])
+@pytest.mark.parametrize("env", [{"HELM_TMA": "0"}, {"HELM_TMA_MZ": "0"}, {"HELM_PLANE_PY": "2"},
+                                 {"HELM_SPLIT": "0"}, {"HELM_SPLIT": "2"}, {"HELM_SPLIT": "2", "HELM_SPLIT_OCC": "4"},
+                                 {"HELM_SPLIT": "2", "HELM_SPLIT_D": "2"}],
+                         ids=["cpasync", "tma_tiles_only", "py2", "single_ring", "split_all", "split_nf3", "split_d2"])
 def test_alternative_stage_paths_match_oracle(env):
     e = dict(os.environ, PYTHONPATH=ROOT + os.pathsep + os.environ.get("PYTHONPATH", ""), **env)
     r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
