@@ -462,7 +462,7 @@ def cpu_baseline_cfg4(alg_bytes_per_solve=None):
            "all_cores": {"value": round(2 * ntask / wall, 4), "unit": "solves/s", "cores": cores,
                          "sample": f"{ntask} single-source replica misfit+gradient evaluations (LU each) in {cores} "
                                    f"processes, {wall:.2f} s wall"},
-           "fullsize_spmv": {"workload": "cfg4 220^3 c128, assembled CSR (74.2 M nonzeros), 1 thread",
+           "fullsize_spmv": {"workload": f"cfg4 {p.next[0]}^3 c128, assembled CSR ({H.nnz / 1e6:.1f} M nonzeros), 1 thread",
                              "gpts": round(p.n_ext / t_spmv / 1e9, 4), "gb_s_alg": round(spmv_gbs, 2),
                              "ms": round(1e3 * t_spmv, 1), "assembly_s": round(t_asm, 1)}}
     if alg_bytes_per_solve:

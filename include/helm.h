@@ -241,8 +241,9 @@ helm_status helm_transfer(helm_op* op, int32_t level, int32_t prolong, int32_t n
 /* Kernel classes: 0 stencil (y = H x), 1 stencil-residual (r = b - H x, ||r||), 2 norm,
  * 3 arnoldi (stencil + CGS projections; the fused GMRES step), 4 update (+norm, Givens),
  * 5 solution update, 6 copy/convert, 7 restrict, 8 prolong-add, 9 fwi (inject/gather/
- * gradient/fold), 10 setup. */
-#define HELM_NCLASS 11
+ * gradient/fold), 10 setup, 11 vcycle_persist (a whole coarse V-cycle in one grid-synchronous
+ * launch, counted at its finer level). */
+#define HELM_NCLASS 12
 
 /* When enable != 0, every `stride`-th launch of each class is bracketed by CUDA events
  * recorded on the stream it is launched on. Resets the accumulated statistics. */

@@ -116,10 +116,82 @@ def extend(prob, m_int: np.ndarray) -> np.ndarray:
     return (extension_matrix(prob) @ np.asarray(m_int, np.float64).ravel()).reshape(ext_shape(prob))
 
 
+# ----------------------------------------------------------------------------- R34 / R35
+# The paper's higher-order stencils (2D "9pt optimal" [23], 3D "compact 27-pt" [60];
+# coefficients not printed): DESIGN readings R34 (2D) / R35 (3D) define them as product forms
+# of 1D operators, so that the PML enters through the same stretched tables T_a as STD2:
+#   L = sum of consistent Laplacians (T_a along one axis times averages A_b along the others),
+#   H = L + omega^2 M diag(E m)          (Eq. 7 with A = M)
+# with A_a = (1/4, 1/2, 1/4) and E_a = (1/2, 0, 1/2) (zero ghosts, R7) and the weights
+# below (derived by scripts/derive_opt_stencil.py: least-squares phase-velocity error over
+# all directions and 4..inf points per wavelength, non-negative weights), copied from DESIGN.
+OPT9 = dict(a=0.58547, c=0.63353, d=0.36647)                       # e = 1 - c - d = 0
+OPT27 = dict(w1=0.36027, w2=0.46886, w3=0.17087, m1=0.47314, m2=0.50415, m3=0.02271)   # m4 = 0
+
+
+def averaging_1d(N: int, w_off: float, w_mid: float) -> sp.csr_matrix:
+    """Tridiagonal (w_off, w_mid, w_off) with zero ghosts: A_a = (1/4, 1/2, 1/4), E_a = (1/2, 0, 1/2)."""
+    return sp.diags([np.full(N - 1, w_off), np.full(N, w_mid), np.full(N - 1, w_off)], [-1, 0, 1],
+                    shape=(N, N), format="csr", dtype=np.complex128)
+
+
+def _k3(Az, Ay, Ax):
+    return sp.kron(Az, sp.kron(Ay, Ax))
+
+
+def operator_from_tables(T, m_ext, omega: float, ndim: int, stencil: str = "std2") -> sp.csr_matrix:
+    """H from the per-axis stretched second differences T = (Tx, Ty, Tz) (Ty None in 2D) and the
+    extended model (C-order [z][y][x]): D5 for "std2", R34 / R35 for "opt"."""
+    Tx, Ty, Tz = T
+    Nx, Nz = Tx.shape[0], Tz.shape[0]
+    Ny = Ty.shape[0] if ndim == 3 else 1
+    Ix, Iy, Iz = (sp.identity(k, format="csr", dtype=np.complex128) for k in (Nx, Ny, Nz))
+    m_diag = sp.diags(omega**2 * np.asarray(m_ext).ravel())
+    if stencil == "std2":
+        L = _k3(Iz, Iy, Tx) + _k3(Tz, Iy, Ix)
+        if ndim == 3:
+            L = L + _k3(Iz, Ty, Ix)
+        return (L + m_diag).tocsr()
+    if stencil != "opt":
+        raise ValueError(f"unknown stencil {stencil!r}")
+    Ax, Az = averaging_1d(Nx, 0.25, 0.5), averaging_1d(Nz, 0.25, 0.5)
+    Ex, Ez = averaging_1d(Nx, 0.5, 0.0), averaging_1d(Nz, 0.5, 0.0)
+    if ndim == 2:
+        a, c, d = OPT9["a"], OPT9["c"], OPT9["d"]
+        e = 1.0 - c - d
+        L = a * (_k3(Iz, Iy, Tx) + _k3(Tz, Iy, Ix)) + (1 - a) * (_k3(Az, Iy, Tx) + _k3(Tz, Iy, Ax))
+        M = c * _k3(Iz, Iy, Ix) + d / 2 * (_k3(Iz, Iy, Ex) + _k3(Ez, Iy, Ix)) + e * _k3(Ez, Iy, Ex)
+        return (L + M @ m_diag).tocsr()
+    Ay, Ey = averaging_1d(Ny, 0.25, 0.5), averaging_1d(Ny, 0.5, 0.0)
+    w1, w2, w3 = OPT27["w1"], OPT27["w2"], OPT27["w3"]
+    m1, m2, m3 = OPT27["m1"], OPT27["m2"], OPT27["m3"]
+    m4 = 1.0 - m1 - m2 - m3
+    L1 = _k3(Iz, Iy, Tx) + _k3(Iz, Ty, Ix) + _k3(Tz, Iy, Ix)
+    L2 = 0.5 * (_k3(Iz, Ay, Tx) + _k3(Az, Iy, Tx) + _k3(Iz, Ty, Ax) + _k3(Az, Ty, Ix) + _k3(Tz, Iy, Ax) + _k3(Tz, Ay, Ix))
+    L3 = _k3(Az, Ay, Tx) + _k3(Az, Ty, Ax) + _k3(Tz, Ay, Ax)
+    L = w1 * L1 + w2 * L2 + w3 * L3
+    M = (m1 * _k3(Iz, Iy, Ix) + m2 / 3 * (_k3(Iz, Iy, Ex) + _k3(Iz, Ey, Ix) + _k3(Ez, Iy, Ix))
+         + m3 / 3 * (_k3(Iz, Ey, Ex) + _k3(Ez, Iy, Ex) + _k3(Ez, Ey, Ix)) + m4 * _k3(Ez, Ey, Ex))
+    return (L + M @ m_diag).tocsr()
+
+
+def mass_matrix(prob) -> sp.csr_matrix:
+    """A of Eq. (7): I for STD2, the mass distribution M of R34 / R35 for "opt"."""
+    Nx, Ny, Nz = prob.next
+    zero = [sp.csr_matrix((k, k), dtype=np.complex128) for k in (Nx, Ny, Nz)]
+    T = (zero[0], zero[1] if prob.ndim == 3 else None, zero[2])
+    return operator_from_tables(T, np.ones(prob.n_ext), 1.0, prob.ndim, stencil_of(prob)).real.tocsr()
+
+
+def stencil_of(prob) -> str:
+    return getattr(prob, "stencil", "std2")
+
+
 # ----------------------------------------------------------------------------- D5
 def helmholtz_matrix(prob, omega: float, pml: PmlParams, m_int: Optional[np.ndarray] = None,
                      ) -> sp.csr_matrix:
-    """D5: H = sum_a T_a (acting along axis a) + omega^2 diag(E m), C-order [z][y][x].
+    """D5: H = sum_a T_a (acting along axis a) + omega^2 diag(E m), C-order [z][y][x] (STD2);
+    prob.stencil == "opt": R34 / R35 (operator_from_tables).
 
     2D problems (ndim == 2) have no y term (ny = 1 and no T_y)."""
     m_int = prob.m if m_int is None else m_int
@@ -128,13 +200,8 @@ def helmholtz_matrix(prob, omega: float, pml: PmlParams, m_int: Optional[np.ndar
     (wxl, wxh), (wyl, wyh), (wzl, wzh) = prob.pml
     Tx = second_difference(*tables_1d(Nx, nx, prob.h, wxl, wxh, omega, pml))
     Tz = second_difference(*tables_1d(Nz, nz, prob.h, wzl, wzh, omega, pml))
-    Ix, Iy, Iz = (sp.identity(k, format="csr", dtype=np.complex128) for k in (Nx, Ny, Nz))
-    L = sp.kron(Iz, sp.kron(Iy, Tx)) + sp.kron(Tz, sp.kron(Iy, Ix))
-    if prob.ndim == 3:
-        Ty = second_difference(*tables_1d(Ny, ny, prob.h, wyl, wyh, omega, pml))
-        L = L + sp.kron(Iz, sp.kron(Ty, Ix))
-    m_ext = extend(prob, m_int).ravel()
-    return (L + sp.diags(omega**2 * m_ext)).tocsr()
+    Ty = second_difference(*tables_1d(Ny, ny, prob.h, wyl, wyh, omega, pml)) if prob.ndim == 3 else None
+    return operator_from_tables((Tx, Ty, Tz), extend(prob, m_int), omega, prob.ndim, stencil_of(prob))
 
 
 def helmholtz_rows(prob, omega: float, pml: PmlParams, z_lo: int, z_hi: int,

@@ -16,8 +16,23 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .discretize import PmlParams, extension_matrix, helmholtz_matrix, interior_to_ext_index
+from .discretize import PmlParams, extension_matrix, helmholtz_matrix, interior_to_ext_index, mass_matrix, stencil_of
 from .solve import LU
+
+
+def _mass_h(prob, V: np.ndarray) -> np.ndarray:
+    """A^H V with A of Eq. (7): identity for STD2, the mass distribution of R34 / R35
+    for the "opt" stencils (the gradient T^* = omega^2 diag(conj u) A^H)."""
+    if stencil_of(prob) == "std2":
+        return V
+    return mass_matrix(prob).conj().T @ V
+
+
+def _mass(prob, X: np.ndarray) -> np.ndarray:
+    """A X (T dm = omega^2 A (u .* E dm), Eq. 7)."""
+    if stencil_of(prob) == "std2":
+        return X
+    return mass_matrix(prob) @ X
 
 
 def source_matrix(prob, omega: float, src_ids: Sequence[int], weight: complex = 1.0) -> np.ndarray:
@@ -73,7 +88,7 @@ def misfit_grad(prob, pml: PmlParams, d_obs: np.ndarray, m_int=None, src_ids=Non
         r = receivers(prob, U) - d_obs[fi].T                             # P_r u - d
         f += 0.5 * float(np.sum(np.abs(r) ** 2))                          # Eq. (2)
         V = lu.solve(-receivers_adjoint(prob, r), adjoint=True)          # v = H^-H(-P_r^T r)
-        g_ext += np.sum(np.real(w**2 * np.conj(U) * V), axis=1)          # Re(w^2 conj(u) v)
+        g_ext += np.sum(np.real(w**2 * np.conj(U) * _mass_h(prob, V)), axis=1)   # Re(w^2 conj(u) A^H v)
         if return_fields:
             fields.append((U, V))
     g = E.T @ g_ext                                                      # E^T (R11)
@@ -84,9 +99,10 @@ def misfit_grad(prob, pml: PmlParams, d_obs: np.ndarray, m_int=None, src_ids=Non
 
 # ----------------------------------------------------------------------------- SURVEY §8(f) rank 1
 # Linearised modelling, its adjoint and the Gauss-Newton Hessian (Table 1, Table 2
-# P:111-117; Listing 1 JACOBI_FORW / JACOBI_ADJ / HESS_GN P:167-180). With A = I (STD2, Eq. 7):
-#   T dm  = DH(m)[dm] u = omega^2 u (.) (E dm)
-#   T^* z = E^T Re(omega^2 conj(u) (.) z)     (sum_srcs = to_phys * real)
+# P:111-117; Listing 1 JACOBI_FORW / JACOBI_ADJ / HESS_GN P:167-180). With A of Eq. 7 (I for
+# STD2, the mass distribution M for the R34 / R35 stencils):
+#   T dm  = DH(m)[dm] u = omega^2 A (u (.) (E dm))
+#   T^* z = E^T Re(omega^2 conj(u) (.) (A^H z))     (sum_srcs = to_phys * real)
 #   J dm  = P_r Du[dm],  Du[dm] = -H^-1 T dm
 #   J^H y = T^* H^-H (-P_r^T y)
 #   H_GN dm = J^H J dm = T^* H^-H (-P_r^T P_r (-H^-1 T dm))
@@ -102,7 +118,7 @@ def jacobian(prob, pml: PmlParams, dm: np.ndarray, m_int=None, src_ids=None, wei
         S = 1.0 if weights is None else weights[fi]
         lu = LU(helmholtz_matrix(prob, w, pml, m_int))
         U = lu.solve(source_matrix(prob, w, src_ids, S))
-        dU = lu.solve(-(w**2) * U * dm_ext[:, None])
+        dU = lu.solve(-(w**2) * _mass(prob, U * dm_ext[:, None]))
         out.append(receivers(prob, dU).T)
     return np.stack(out)
 
@@ -117,7 +133,7 @@ def jacobian_adjoint(prob, pml: PmlParams, y: np.ndarray, m_int=None, src_ids=No
         lu = LU(helmholtz_matrix(prob, w, pml, m_int))
         U = lu.solve(source_matrix(prob, w, src_ids, S))
         V = lu.solve(-receivers_adjoint(prob, y[fi].T), adjoint=True)
-        g_ext += np.sum(np.real(w**2 * np.conj(U) * V), axis=1)
+        g_ext += np.sum(np.real(w**2 * np.conj(U) * _mass_h(prob, V)), axis=1)
     return (extension_matrix(prob).T @ g_ext).reshape(prob.m.shape)
 
 
@@ -131,9 +147,9 @@ def gn_hessian(prob, pml: PmlParams, dm: np.ndarray, m_int=None, src_ids=None, w
         S = 1.0 if weights is None else weights[fi]
         lu = LU(helmholtz_matrix(prob, w, pml, m_int))
         U = lu.solve(source_matrix(prob, w, src_ids, S))
-        dU = lu.solve(-(w**2) * U * dm_ext[:, None])
+        dU = lu.solve(-(w**2) * _mass(prob, U * dm_ext[:, None]))
         V = lu.solve(-receivers_adjoint(prob, receivers(prob, dU)), adjoint=True)
-        g_ext += np.sum(np.real(w**2 * np.conj(U) * V), axis=1)
+        g_ext += np.sum(np.real(w**2 * np.conj(U) * _mass_h(prob, V)), axis=1)
     return (extension_matrix(prob).T @ g_ext).reshape(prob.m.shape)
 
 

@@ -27,7 +27,7 @@ from typing import Callable, List, Optional
 import numpy as np
 import scipy.sparse as sp
 
-from .discretize import PmlParams, extend, second_difference, tables_1d
+from .discretize import PmlParams, extend, operator_from_tables, second_difference, stencil_of, tables_1d
 
 BREAKDOWN = 1e-14
 
@@ -112,12 +112,8 @@ class Hierarchy:
         nx, ny, nz = pr.n
         Tx = second_difference(*tables_1d(Nx, nx, pr.h, wxl, wxh, self.omega, self.pml, l))
         Tz = second_difference(*tables_1d(Nz, nz, pr.h, wzl, wzh, self.omega, self.pml, l))
-        Ix, Iy, Iz = (sp.identity(k, format="csr", dtype=np.complex128) for k in (Nx, Ny, Nz))
-        L = sp.kron(Iz, sp.kron(Iy, Tx)) + sp.kron(Tz, sp.kron(Iy, Ix))
-        if self.d == 3:
-            Ty = second_difference(*tables_1d(Ny, ny, pr.h, wyl, wyh, self.omega, self.pml, l))
-            L = L + sp.kron(Iz, sp.kron(Ty, Ix))
-        return (L + sp.diags(self.omega**2 * self.m_ext[l].ravel())).tocsr()
+        Ty = second_difference(*tables_1d(Ny, ny, pr.h, wyl, wyh, self.omega, self.pml, l)) if self.d == 3 else None
+        return operator_from_tables((Tx, Ty, Tz), self.m_ext[l], self.omega, self.d, stencil_of(pr))
 
     def op(self, l: int, adjoint: bool) -> Callable[[np.ndarray], np.ndarray]:
         A = self.HH[l] if adjoint else self.H[l]

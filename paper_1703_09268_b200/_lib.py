@@ -48,9 +48,9 @@ class HelmSolveReport(C.Structure):
 
 HELM_OK, HELM_ERR_ARG, HELM_ERR_SHAPE, HELM_ERR_CUDA, HELM_ERR_OOM, HELM_ERR_STATE = 0, -1, -2, -3, -4, -5
 HELM_C64, HELM_C128 = 0, 1
-NCLASS = 11
+NCLASS = 12
 CLASS_NAMES = ["stencil", "stencil_resid", "norm", "arnoldi", "update", "solupdate", "copy", "restrict",
-               "prolong_add", "fwi", "setup"]
+               "prolong_add", "fwi", "setup", "vcycle_persist"]
 
 _P = C.c_void_p
 _d = C.POINTER(C.c_double)

@@ -8,7 +8,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "helm.cu")]
-DEPS = SRC + [os.path.join(PKG, "csrc", f) for f in ("common.cuh", "kernels.cuh", "stencil.cuh", "march2d.cuh")] + \
+DEPS = SRC + [os.path.join(PKG, "csrc", f) for f in ("common.cuh", "kernels.cuh", "stencil.cuh", "march2d.cuh", "persist.cuh")] + \
     [os.path.join(ROOT, "include", "helm.h")]
 LIB = os.path.join(PKG, "lib", "libhelm.so")
 

@@ -3,6 +3,7 @@
 // declared in include/helm.h. All numerics run in the kernels of kernels.cuh.
 #include "helm.h"
 #include "march2d.cuh"
+#include "persist.cuh"
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -46,7 +47,7 @@ constexpr int K1 = HELM_KMAX + 1;
 
 // ------------------------------------------------------------------------------ probes
 enum KClass { KC_STENCIL = 0, KC_RESID, KC_NORM, KC_DOTS, KC_UPDATE, KC_SOLUPD, KC_COPY, KC_RESTRICT,
-              KC_PROLONG, KC_FWI, KC_SETUP };
+              KC_PROLONG, KC_FWI, KC_SETUP, KC_PERSIST };
 struct ProbeRec { int cls, level; cudaEvent_t a, b; double bytes; };
 struct Prof {
   bool on = false;
@@ -826,9 +827,92 @@ template <typename R> LevelWS<R>* wsets(helm_op* op);
 template <> LevelWS<double>* wsets<double>(helm_op* op) { return op->w64; }
 template <> LevelWS<float>* wsets<float>(helm_op* op) { return op->w32; }
 
+// Algorithmic bytes of one persistent-kernel GMRES(ko, ki) on N points (its own schedule:
+// per step a stencil+projection pass and an update+norm pass, then the solution update).
+double persist_gmres_bytes(double N, int ko, int ki, bool x0zero, double Sc, double Sr) {
+  double b = 0.0;
+  for (int c = 0; c < ko; ++c) {
+    const bool zero = x0zero && c == 0;
+    b += zero ? Sc * N : (3 * Sc + Sr) * N;                         // r = b - H x, ||r||
+    for (int j = 0; j < ki; ++j) b += (2.0 * (j + 3) * Sc + Sr) * N;  // both passes of step j
+    b += (ki + (zero ? 1 : 2)) * Sc * N;                              // x update
+  }
+  return b;
+}
+
+// The V-cycle at the second-to-last level (l + 1 coarsest) as ONE cooperative launch
+// (persist.cuh) when the level is small (HELM_PERSIST_MAXPTS points over the active RHS,
+// default 2^21). OPT-IN (HELM_PERSIST=1): measured on the B200 (profiles/r02/persist_ab.txt)
+// it issues 10x fewer launches but is not faster — cfg3 one solve 148 vs 137 ms, 8-source
+// batch 306 vs 217 ms, cfg2 bench 31 vs 66 solves/s — because a grid barrier plus the
+// dependent L2 round trips of a pass cost about what a graph-launched kernel boundary does
+// (DESIGN §6, §11). Returns false when not applicable.
+template <typename R>
+bool vcycle_persist(helm_op* op, int l, int adj, int nrhs, const cx<R>* b, cx<R>* x) {
+  static const int on = env_int("HELM_PERSIST", 0);
+  static const long long maxpts = std::max(0, env_int("HELM_PERSIST_MAXPTS", 1 << 21));
+  if (!on || op->nact == 0 || l + 1 != op->L - 1) return false;
+  const LevelDev &F = op->lev[l], &Cc = op->lev[l + 1];
+  if (F.N * (long long)op->nact > maxpts) return false;
+  const helm_mlopts& o = op->ml;
+  constexpr int NT = 256;
+  auto kern = k_vcycle_persist<R, NT>;
+  static const int per_sm = [&] {
+    int v = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, NT, 0));
+    return v;
+  }();
+  const long long G = (long long)per_sm * num_sms();
+  if (per_sm < 1 || G < op->nact) return false;
+  // CTAs per RHS: all co-resident CTAs, but no fewer than 4 x NT fine points per CTA
+  const int cpr = (int)std::max(1LL, std::min(G / op->nact, (F.N + 4 * NT - 1) / (4 * NT)));
+  LevelWS<R>* W = wsets<R>(op);
+  PersistArgs<R> a{};
+  a.gf = geo<R>(op, l, adj);
+  a.gc = geo<R>(op, l + 1, adj);
+  a.b = b; a.x = x;
+  for (int i = 0; i <= o.ks_i; ++i) a.SV[i] = W[l].SV[i];
+  a.SW = W[l].SW;
+  for (int i = 0; i <= o.kc_i; ++i) a.FV[i] = W[l + 1].FV[i];
+  a.FW = W[l + 1].FW; a.Fx = W[l + 1].Fx; a.Fb = W[l + 1].Fb;
+  a.active = op->active_d; a.nact = op->nact; a.cpr = cpr;
+  a.ks_o = o.ks_o; a.ks_i = o.ks_i; a.kc_o = o.kc_o; a.kc_i = o.kc_i;
+  a.has_y = op->dim == 3; a.fac = (R)std::ldexp(1.0, -op->dim);
+  a.part = op->rb.part;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(op->nact * cpr));
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = op->st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const double Sc = sizeof(cx<R>), Sr = sizeof(R);
+  const double bytes = persist_gmres_bytes((double)F.N, o.ks_o, o.ks_i, true, Sc, Sr) +
+                       persist_gmres_bytes((double)F.N, o.ks_o, o.ks_i, false, Sc, Sr) +
+                       (3 * Sc + Sr) * F.N + Sc * (F.N + Cc.N) +                  // residual, restrict
+                       persist_gmres_bytes((double)Cc.N, o.kc_o, o.kc_i, true, Sc, Sr) +
+                       Sc * (2.0 * F.N + Cc.N);                                    // prolong + add
+  prof_begin(KC_PERSIST, op->st, l);
+  CK(cudaLaunchKernelEx(&cfg, kern, a));
+  CKL();
+  prof_end(KC_PERSIST, op->st, acct(op, l, bytes, false, nrhs));
+  // matvec counts of the equivalent launch sequence: per GMRES(ko, ki) ko ki steps plus the
+  // restart residuals, plus the V-cycle residual at level l
+  for (int r = 0; r < nrhs; ++r)
+    if (op->act_h[r]) {
+      op->mv[l][r] += 2LL * o.ks_o * o.ks_i + (o.ks_o - 1) + o.ks_o + 1;
+      op->mv[l + 1][r] += (long long)o.kc_o * o.kc_i + (o.kc_o - 1);
+    }
+  return true;
+}
+
 // Alg. 1 with the recursion of Fig. 3: x = M_l(b).
 template <typename R>
 void vcycle(helm_op* op, int l, int adj, int nrhs, const cx<R>* b, cx<R>* x) {
+  if (vcycle_persist<R>(op, l, adj, nrhs, b, x)) return;
   LevelWS<R>* W = wsets<R>(op);
   const helm_mlopts& o = op->ml;
   // pre-smooth: GMRES(ks_o, ks_i) from 0 (R19)

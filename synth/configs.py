@@ -31,6 +31,7 @@ class Problem:
     src: np.ndarray                         # int64 interior node ids
     rec: np.ndarray                         # int64 interior node ids
     m_true: Optional[np.ndarray] = None     # model that generated observed data
+    stencil: str = "std2"                    # discretisation: "std2" (5/7-pt) or "opt" (9/27-pt, R34/R35)
 
     @property
     def next(self) -> Tuple[int, int, int]:

@@ -3,7 +3,9 @@ read once per process): per-thread cp.async instead of TMA (HELM_TMA=0), TMA til
 the z coefficients by cp.async (HELM_TMA_MZ=0), and two rows per thread for the matvec
 (HELM_PLANE_PY=2), the single-ring fused Arnoldi steps everywhere (HELM_SPLIT=0), the split
 ring for every fused step (HELM_SPLIT=2), also with three formed slots (two barriers per
-plane, HELM_SPLIT_OCC=4) or two raw stages (HELM_SPLIT_D=2). Each must match the assembled oracle H (c128 <= 1e-12, c64 <= 1e-5) for
+plane, HELM_SPLIT_OCC=4) or two raw stages (HELM_SPLIT_D=2), and coarse V-cycles as kernel
+one grid-synchronous launch instead of a launch sequence (HELM_PERSIST=1; the level-1
+V-cycle is also compared with the numpy mirror, <= 1e-12, and must take <= 2 launches). Each must match the assembled oracle H (c128 <= 1e-12, c64 <= 1e-5) for
 helm_apply forward / adjoint on a ragged multi-tile grid, and give a certified solve."""
 import json
 import os
@@ -45,14 +47,28 @@ for name, dt, td in (("c128", api.C128, torch.complex128), ("c64", api.C64, torc
     Xh = X.cpu().numpy().astype(np.complex128)
     out[f"{name}_solve"] = max(rel_residual(H, Xh[r], b[r]) for r in range(3))
     out[f"{name}_conv"] = all(r["converged"] for r in rep)
+# level-1 V-cycle (coarsest GMRES below it) vs the mirror, complex128
+from oracle import mlgmres
+op = api.helm_setup(api.Grid.of(p), p.m, w, api.Pml(pml.R, pml.power, pml.v_ref), api.C128, max_rhs=2)
+hier = mlgmres.Hierarchy(p, w, pml)
+n1 = int(np.prod(hier.shapes[1]))
+b1 = synth.random_complex((2, n1), 2)
+z1 = torch.zeros(2, n1, dtype=torch.complex128, device="cuda")
+l0 = api.launch_count()
+api.helm_vcycle(op, torch.from_numpy(b1).cuda(), z1, level=1, adjoint=1)
+out["vcycle1_launches"] = api.launch_count() - l0
+zg = z1.cpu().numpy()
+out["vcycle1"] = max(float(np.linalg.norm(zg[r] - mlgmres.vcycle(hier, 1, b1[r], adjoint=True)) /
+                          np.linalg.norm(zg[r])) for r in range(2))
 print(json.dumps(out))
 """
 
 
 @pytest.mark.parametrize("env", [{"HELM_TMA": "0"}, {"HELM_TMA_MZ": "0"}, {"HELM_PLANE_PY": "2"},
                                  {"HELM_SPLIT": "0"}, {"HELM_SPLIT": "2"}, {"HELM_SPLIT": "2", "HELM_SPLIT_OCC": "4"},
-                                 {"HELM_SPLIT": "2", "HELM_SPLIT_D": "2"}],
-                         ids=["cpasync", "tma_tiles_only", "py2", "single_ring", "split_all", "split_nf3", "split_d2"])
+                                 {"HELM_SPLIT": "2", "HELM_SPLIT_D": "2"}, {"HELM_PERSIST": "1"}],
+                         ids=["cpasync", "tma_tiles_only", "py2", "single_ring", "split_all", "split_nf3", "split_d2",
+                              "persistent_vcycle"])
 def test_alternative_stage_paths_match_oracle(env):
     e = dict(os.environ, PYTHONPATH=ROOT + os.pathsep + os.environ.get("PYTHONPATH", ""), **env)
     r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
@@ -63,3 +79,6 @@ def test_alternative_stage_paths_match_oracle(env):
         assert res[f"c64_apply{adj}"] <= 1e-5, res
     assert res["c128_conv"] and res["c128_solve"] <= 1e-6 * (1 + 1e-3), res
     assert res["c64_conv"] and res["c64_solve"] <= 2e-6, res
+    assert res["vcycle1"] <= 1e-12, res
+    if env.get("HELM_PERSIST") == "1":
+        assert res["vcycle1_launches"] <= 2, res

@@ -59,6 +59,23 @@ def test_vcycle_matches_mirror(make, adjoint):
         assert rel(zg[r], ref) <= 1e-12
 
 
+@pytest.mark.parametrize("make,adjoint,nrhs", [(synth.tiny2d, 0, 2), (synth.tiny3d, 1, 2), (synth.cfg1, 0, 1),
+                                                (synth.cfg1, 1, 3)])
+def test_coarse_vcycle_matches_mirror(make, adjoint, nrhs):
+    """The V-cycle at the second-to-last level (coarsest GMRES below it), same fixed counts as
+    the mirror (the grid-synchronous single-launch variant is checked in test_gpu_paths)."""
+    p = make()
+    op, w, pml = _setup(p, nrhs=nrhs)
+    hier = mlgmres.Hierarchy(p, w, pml)
+    n1 = int(np.prod(hier.shapes[1]))
+    b = synth.random_complex((nrhs, n1), 2)
+    z = torch.zeros(nrhs, n1, dtype=torch.complex128, device="cuda")
+    api.helm_vcycle(op, to_dev(b), z, level=1, adjoint=adjoint)
+    zg = to_host(z)
+    for r in range(nrhs):
+        assert rel(zg[r], mlgmres.vcycle(hier, 1, b[r], adjoint=bool(adjoint))) <= 1e-12
+
+
 @pytest.mark.parametrize("dtype", [api.C128, api.C64])
 def test_cfg1_solve_matches_lu_and_green(dtype):
     """Config 1 (BASELINE configs[0]): vs LU <= 1e-5, certificate <= 1e-6, vs -(i/4)H0 <= 1.5 %."""
