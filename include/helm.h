@@ -55,7 +55,17 @@ typedef struct {
   int64_t n[3];        /* interior points per axis, x first (n[1] = 1 in 2D) */
   double h;            /* uniform spacing [m], > 0 */
   int32_t pml[3][2];   /* PML points per axis per side (pml[1] = {0,0} in 2D) */
+  int32_t stencil;     /* HELM_STD2 (0): 5-pt (2D) / 7-pt (3D), D4-D5 (R4). HELM_OPT (1): the paper's
+                        * higher-order stencils ("9pt optimal" [23] / "compact 27-pt" [60]) as
+                        * DESIGN R34 (2D 9-pt) / R35 (3D 27-pt): product forms of the same stretched
+                        * 1D tables, H = L + omega^2 M diag(m) with the mass distribution M = A of
+                        * Eq. (7). Every level of the hierarchy uses the same kind. OPT is
+                        * supported by helm_apply, helm_solve, fwi_misfit_grad, fwi_forward and
+                        * fwi_jacobian_adjoint; the Born-source calls (fwi_jacobian,
+                        * fwi_gn_hessian) and off-grid acquisition return HELM_ERR_ARG for it. */
 } helm_grid;
+#define HELM_STD2 0
+#define HELM_OPT 1
 
 /* D3 / R5. sigma(d) = sigma_max (d/L)^power, sigma_max = (power+1) v_ref ln(1/R) / (2L),
  * eta = 1 + i sigma/omega (R3). v_ref <= 0 in helm_setup means "max velocity of m";

@@ -16,7 +16,8 @@ if os.environ.get("HELM_LIB_VARIANT"):
 
 
 class HelmGrid(C.Structure):
-    _fields_ = [("ndim", C.c_int32), ("n", C.c_int64 * 3), ("h", C.c_double), ("pml", (C.c_int32 * 2) * 3)]
+    _fields_ = [("ndim", C.c_int32), ("n", C.c_int64 * 3), ("h", C.c_double), ("pml", (C.c_int32 * 2) * 3),
+                ("stencil", C.c_int32)]
 
 
 class HelmPml(C.Structure):
@@ -48,6 +49,7 @@ class HelmSolveReport(C.Structure):
 
 HELM_OK, HELM_ERR_ARG, HELM_ERR_SHAPE, HELM_ERR_CUDA, HELM_ERR_OOM, HELM_ERR_STATE = 0, -1, -2, -3, -4, -5
 HELM_C64, HELM_C128 = 0, 1
+HELM_STD2, HELM_OPT = 0, 1
 NCLASS = 12
 CLASS_NAMES = ["stencil", "stencil_resid", "norm", "arnoldi", "update", "solupdate", "copy", "restrict",
                "prolong_add", "fwi", "setup", "vcycle_persist"]

@@ -20,17 +20,23 @@ C64, C128 = L.HELM_C64, L.HELM_C128
 TORCH_DTYPE = {C64: torch.complex64, C128: torch.complex128}
 
 
+STENCILS = {"std2": L.HELM_STD2, "opt": L.HELM_OPT}
+
+
 @dataclasses.dataclass(frozen=True)
 class Grid:
-    """D1: interior sizes (nx, ny, nz) (ny = 1 in 2D), spacing h, PML ((xl,xh),(yl,yh),(zl,zh))."""
+    """D1: interior sizes (nx, ny, nz) (ny = 1 in 2D), spacing h, PML ((xl,xh),(yl,yh),(zl,zh)),
+    stencil "std2" (5/7-pt, D4-D5) or "opt" (9/27-pt, DESIGN R34/R35)."""
     ndim: int
     n: Tuple[int, int, int]
     h: float
     pml: Tuple[Tuple[int, int], ...]
+    stencil: str = "std2"
 
     @staticmethod
     def of(p) -> "Grid":
-        return Grid(int(p.ndim), tuple(int(v) for v in p.n), float(p.h), tuple(tuple(int(w) for w in a) for a in p.pml))
+        return Grid(int(p.ndim), tuple(int(v) for v in p.n), float(p.h), tuple(tuple(int(w) for w in a) for a in p.pml),
+                    getattr(p, "stencil", "std2"))
 
     @property
     def next(self):
@@ -51,6 +57,7 @@ class Grid:
             g.n[a] = self.n[a]
             g.pml[a][0], g.pml[a][1] = self.pml[a]
         g.h = self.h
+        g.stencil = STENCILS[self.stencil]
         return g
 
 

@@ -263,6 +263,8 @@ template <> Geo<double> geo<double>(const helm_op* op, int l, int adj) {
   for (int o = 0; o < op->nop; ++o) g.w2[o] = op->omegas[o] * op->omegas[o];
   for (int a = 0; a < 3; ++a) { g.lo[a] = L.t64[adj][a][0]; g.dg[a] = L.t64[adj][a][1]; g.up[a] = L.t64[adj][a][2]; }
   g.zpk = L.z64[adj];
+  g.st = op->grid.stencil;
+  g.adj = adj;
   return g;
 }
 template <> Geo<float> geo<float>(const helm_op* op, int l, int adj) {
@@ -273,6 +275,8 @@ template <> Geo<float> geo<float>(const helm_op* op, int l, int adj) {
   for (int o = 0; o < op->nop; ++o) g.w2[o] = (float)(op->omegas[o] * op->omegas[o]);
   for (int a = 0; a < 3; ++a) { g.lo[a] = L.t32[adj][a][0]; g.dg[a] = L.t32[adj][a][1]; g.up[a] = L.t32[adj][a][2]; }
   g.zpk = L.z32[adj];
+  g.st = op->grid.stencil;
+  g.adj = adj;
   return g;
 }
 
@@ -386,7 +390,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
 }
 
 template <typename R>
-bool make_tile_map(CUtensorMap* m, const void* base, int nx, int ny, int nz, int nrhs) {
+bool make_tile_map(CUtensorMap* m, const void* base, int nx, int ny, int nz, int nrhs, int by = 8) {
   auto enc = tma_encoder();
   if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
   // the tensor element is an 8-byte word (one complex64, or half a complex128): TMA only
@@ -398,7 +402,7 @@ bool make_tile_map(CUtensorMap* m, const void* base, int nx, int ny, int nz, int
   // box = the tile plus its x halo, starting 16-B aligned (PlaneSmem::XO): 34 complex128 or
   // 36 complex64 per row
   const cuuint32_t xo = (cuuint32_t)(16 / sizeof(cx<R>));
-  cuuint32_t box[4] = {(cuuint32_t)((32 + 2 * xo) * ce), 10, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)((32 + 2 * xo) * ce), (cuuint32_t)(by + 2), 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   const CUresult rc = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, es,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -409,12 +413,15 @@ bool make_tile_map(CUtensorMap* m, const void* base, int nx, int ny, int nz, int
 // TMA maps of the per-plane operands that are not halo'd: m (16-B pitched copy, box = the
 // 32 x 8 own points of a tile) and the padded z-coefficient rows (box = one plane's 4 entries).
 template <typename R>
-bool make_m_map(CUtensorMap* m, const R* mq, int nxq, int ny, int nz) {
+bool make_m_map(CUtensorMap* m, const R* mq, int nxq, int ny, int nz, bool halo = false, int by = 8) {
   auto enc = tma_encoder();
   if (!enc || !mq) return false;
   cuuint64_t dims[3] = {(cuuint64_t)nxq, (cuuint64_t)ny, (cuuint64_t)nz};
   cuuint64_t strides[2] = {(cuuint64_t)nxq * sizeof(R), (cuuint64_t)nxq * ny * sizeof(R)};
-  cuuint32_t box[3] = {32, 8, 1};
+  // own points (32 x 8), or for the OPT stencils' mass term the halo'd tile starting 16 B
+  // before the interior (PlaneSmem::XOm) and one row above: (32 + 2 XOm) x 10
+  const cuuint32_t xom = (cuuint32_t)(16 / sizeof(R));
+  cuuint32_t box[3] = {halo ? 32 + 2 * xom : 32, (cuuint32_t)(halo ? by + 2 : by), 1};
   cuuint32_t es[3] = {1, 1, 1};
   return enc(m, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
              const_cast<R*>(mq), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -461,16 +468,21 @@ PlaneSplit plane_split(int groups, long long G, int T, int nz) {
 }
 
 // Launch with exactly one resident wave (groups x cpg CTAs, see stencil.cuh).
-template <typename R, int MODE, int NV, bool YC, int PY = plane_py<MODE, YC>(), bool SPLIT = false>
+template <typename R, int MODE, int NV, bool YC, int PY = plane_py<MODE, YC>(), bool SPLIT = false, int ST = 0,
+          int BY = 8>
 void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
-  if constexpr (MODE == 0 && PY == 4) {   // HELM_PLANE_PY=2: two rows per thread (A/B)
-    static const bool py2 = env_int("HELM_PLANE_PY", 4) == 2;
+  if constexpr (MODE == 0 && PY == 4 && ST == 0 && BY == 8) {   // A/B switches of the matvec
+    static const bool py2 = env_int("HELM_PLANE_PY", 4) == 2;    // two rows per thread
     if (py2) { run_plane<R, MODE, NV, YC, 2>(a, groups, units, st); return; }
+    if (a.by == 16) {                                             // launch_plane chose 16-row tiles
+      run_plane<R, MODE, NV, YC, 4, false, 0, 16>(a, groups, units, st);
+      return;
+    }
   }
   using Sh = PlaneShape<MODE, NV>;
-  constexpr int NT = 32 * 8 / PY;
-  constexpr size_t sb = PlaneSmem<R, 32, 8, Sh::NX, Sh::NP, YC, SPLIT>::stage_bytes;
-  auto kern = k_plane<R, 32, 8, PY, MODE, NV, YC, SPLIT>;
+  constexpr int NT = 32 * BY / PY;
+  constexpr size_t sb = PlaneSmem<R, 32, BY, Sh::NX, Sh::NP, YC, SPLIT, ST == 1>::stage_bytes;
+  auto kern = k_plane<R, 32, BY, PY, MODE, NV, YC, SPLIT, ST>;
   static const PlaneCfg cfg = [&] {
     PlaneCfg c;
     const PlaneTune& t = plane_tune<R, PY>();
@@ -507,6 +519,8 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
   a.cpg = sp.cpg; a.nzc = sp.nzc; a.zlen = sp.zlen;
   a.S = cfg.S;
   a.nf = cfg.nf;
+  static const int prev_on = env_int("HELM_PREV", 1);
+  a.prev = prev_on;
   if (env_int("HELM_DEBUG", 0) > 1)
     std::fprintf(stderr, "[helm] plane launch mode=%d nv=%d split=%d groups=%d cpg=%d nzc=%d zlen=%d tiles=%d\n", MODE, NV,
                  (int)SPLIT, groups, sp.cpg, sp.nzc, sp.zlen, a.ntx * a.nty);
@@ -528,9 +542,9 @@ template <typename R> int march_max_ops(int nz) {
 // The per-lane cp.async ring holds S planes (S-2 in flight): S is the largest depth <= 16
 // whose rings fit a shared-memory budget of ~220 KB / occ_target CTAs (5 by default: a
 // shallower ring for up to 20 warps per SM; HELM_MARCH_OCC / HELM_MARCH_S override for tuning).
-template <typename R, int MODE, int NV>
+template <typename R, int MODE, int NV, int ST = 0>
 void run_march(MarchArgs<R>& a, cudaStream_t st) {
-  auto kern = k_march2d<R, MODE, NV>;
+  auto kern = k_march2d<R, MODE, NV, ST>;
   constexpr int SB = MarchShape<R, MODE, NV>::stage_bytes;
   const size_t zbytes = ((size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>) + 15) / 16 * 16;
   // bench A/B (march2d_variants_ab.txt): complex128 5 vs 4 = +3-5 %; complex64 (half the stage
@@ -620,7 +634,13 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
     m.nrhs = op->nact; m.ctx = ctx; m.rb = op->rb;
     m.nstrip = (m.g.nx + 29) / 30;
     prof_begin(cls, op->st, l);
-    if (mode == 0) run_march<R, 0, 0>(m, op->st);
+    if (op->grid.stencil == HELM_OPT) {   // R34: the 9-point stencil
+      if (mode == 0) run_march<R, 0, 0, 1>(m, op->st);
+      else if (mode == 1) run_march<R, 1, 0, 1>(m, op->st);
+      else if (mode == 2) dispatch_k(nv, [&](auto c) { run_march<R, 2, decltype(c)::value, 1>(m, op->st); });
+      else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_march<R, 3, decltype(c)::value, 1>(m, op->st); });
+      else dispatch_k0(nv, [&](auto c) { run_march<R, 4, decltype(c)::value, 1>(m, op->st); });
+    } else if (mode == 0) run_march<R, 0, 0>(m, op->st);
     else if (mode == 1) run_march<R, 1, 0>(m, op->st);
     else if (mode == 2) dispatch_k(nv, [&](auto c) { run_march<R, 2, decltype(c)::value>(m, op->st); });
     else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_march<R, 3, decltype(c)::value>(m, op->st); });
@@ -637,23 +657,47 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
   a.jskip = mode >= 3 ? std::max(nv - 1, 0) : j;
   a.nrhs = nrhs; a.ctx = ctx; a.rb = op->rb;
   a.ntx = (a.g.nx + 31) / 32;
-  a.nty = (a.g.ny + 7) / 8;
+  // tile height: 8 rows; the plain matvec can use 16 (HELM_MATVEC_BY=16: half the y-halo
+  // overhead per point, one CTA covers 32 x 16 points)
+  static const int mv_by = env_int("HELM_MATVEC_BY", 8) == 16 ? 16 : 8;
+  const int by = (mode == 0 && op->grid.stencil == HELM_STD2) ? mv_by : 8;
+  a.nty = (a.g.ny + by - 1) / by;
+  a.by = by;
   const int groups = op->nact;
   // TMA for the halo'd tiles when every halo'd operand can be described (HELM_TMA=0: cp.async)
   static const bool tma_on = env_int("HELM_TMA", 1) != 0;
+  const bool opt = op->grid.stencil == HELM_OPT;
   a.tma = 0;
-  if (tma_on) {
+  if (tma_on || opt) {
     const int nxt = mode >= 3 ? nv + 1 : 1;
     bool ok = true;
     for (int t = 0; t < nxt && ok; ++t)
-      ok = make_tile_map<R>(&a.tm[t], t == 0 ? (const void*)x : (const void*)a.V.p[t - 1], a.g.nx, a.g.ny, a.g.nz, nrhs);
+      ok = make_tile_map<R>(&a.tm[t], t == 0 ? (const void*)x : (const void*)a.V.p[t - 1], a.g.nx, a.g.ny, a.g.nz, nrhs,
+                            by);
     a.tma = ok ? 1 : 0;
-    static const bool tmq_on = env_int("HELM_TMA_MZ", 1) != 0;
+    static const bool tmq_on_env = env_int("HELM_TMA_MZ", 1) != 0;
+    const bool tmq_on = tmq_on_env || opt;
     const LevelDev& Lv = op->lev[l];
-    a.tmq = a.tma && tmq_on && make_m_map<R>(&a.tmm, level_mq<R>(Lv), Lv.nxq, Lv.ny, Lv.nz) &&
+    a.tmq = a.tma && tmq_on && make_m_map<R>(&a.tmm, level_mq<R>(Lv), Lv.nxq, Lv.ny, Lv.nz, opt, by) &&
             make_z_map<R>(&a.tmz, level_zq<R>(Lv, adj), Lv.nz, op->nop);
   }
   const long long units = (long long)a.ntx * a.nty * a.g.nz;
+  if (opt) {   // R35: every mode of the plane kernel on the 27-point stencil (single ring, TMA)
+    REQ(a.tma && a.tmq, HELM_ERR_SHAPE,
+        "the OPT stencil needs TMA-describable rows on every level (complex64: even extended nx)");
+    prof_begin(cls, op->st, l);
+    // one row per thread (256-thread CTAs): the 27-point sum for 4 rows per thread needed 255
+    // registers and 400 B of stack (measured 14 Gpts/s at 512^3 c128)
+    if (mode == 0) run_plane<R, 0, 0, true, 1, false, 1>(a, groups, units, op->st);
+    else if (mode == 1) run_plane<R, 1, 0, true, 1, false, 1>(a, groups, units, op->st);
+    else if (mode == 2)
+      dispatch_k(nv, [&](auto c) { run_plane<R, 2, decltype(c)::value, true, 1, false, 1>(a, groups, units, op->st); });
+    else if (mode == 3) dispatch_k0(nv, [&](auto c) { run_plane<R, 3, decltype(c)::value, true, 1, false, 1>(a, groups, units, op->st); });
+    else dispatch_k0(nv, [&](auto c) { run_plane<R, 4, decltype(c)::value, true, 1, false, 1>(a, groups, units, op->st); });
+    CKL();
+    prof_end(cls, op->st, acct(op, l, per * a.g.N, true, nrhs));
+    return;
+  }
   prof_begin(cls, op->st, l);
   if (mode == 0) run_plane<R, 0, 0, true>(a, groups, units, op->st);
   else if (mode == 1) run_plane<R, 1, 0, true>(a, groups, units, op->st);
@@ -851,7 +895,7 @@ template <typename R>
 bool vcycle_persist(helm_op* op, int l, int adj, int nrhs, const cx<R>* b, cx<R>* x) {
   static const int on = env_int("HELM_PERSIST", 0);
   static const long long maxpts = std::max(0, env_int("HELM_PERSIST_MAXPTS", 1 << 21));
-  if (!on || op->nact == 0 || l + 1 != op->L - 1) return false;
+  if (!on || op->nact == 0 || l + 1 != op->L - 1 || op->grid.stencil != HELM_STD2) return false;
   const LevelDev &F = op->lev[l], &Cc = op->lev[l + 1];
   if (F.N * (long long)op->nact > maxpts) return false;
   const helm_mlopts& o = op->ml;
@@ -1079,6 +1123,7 @@ void validate_grid(const helm_grid* g) {
   if (g->ndim == 2) REQ(g->n[1] == 1 && g->pml[1][0] == 0 && g->pml[1][1] == 0, HELM_ERR_SHAPE, "2D grids need n[1]=1, pml[1]={0,0}");
   else REQ(g->n[1] >= 2, HELM_ERR_SHAPE, "3D grids need n[1] >= 2");
   REQ(g->n[0] >= 2 && g->n[2] >= 2, HELM_ERR_SHAPE, "n[0], n[2] must be >= 2");
+  REQ(g->stencil == HELM_STD2 || g->stencil == HELM_OPT, HELM_ERR_ARG, "stencil must be HELM_STD2 or HELM_OPT");
   for (int a = 0; a < 3; ++a) REQ(g->n[a] + g->pml[a][0] + g->pml[a][1] < (1LL << 30), HELM_ERR_SHAPE, "axis too large");
 }
 
@@ -1197,6 +1242,10 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
       Lv.nxq = (Lv.nx + 3) / 4 * 4;
       Lv.mq64 = dalloc<double>(op->allocs, (size_t)Lv.nxq * Lv.ny * Lv.nz);
       if (dtype == HELM_C64) Lv.mq32 = dalloc<float>(op->allocs, (size_t)Lv.nxq * Lv.ny * Lv.nz);
+      // the row padding [nx, nxq) is read as the x = nx ghost's model by the OPT stencil's
+      // halo'd m tile: keep it finite (zero)
+      CK(cudaMemset(Lv.mq64, 0, sizeof(double) * (size_t)Lv.nxq * Lv.ny * Lv.nz));
+      if (Lv.mq32) CK(cudaMemset(Lv.mq32, 0, sizeof(float) * (size_t)Lv.nxq * Lv.ny * Lv.nz));
     }
   }
   op->m_int_d = dalloc<double>(op->allocs, n_int);
@@ -1779,9 +1828,13 @@ void fwi_run(helm_op* op, const helm_grid& G, FwiMode mode, int nfreq, const dou
     // a8: adjoint solves
     solve_any(op, 1, nb, fb.A, fb.V, so, rtmp.data());
     put_rep(nb, rs - 1);
-    // a9: g_ext += sum_b Re(omega_b^2 conj(u_b) v_b)
+    // a9: g_ext += sum_b Re(omega_b^2 conj(u_b) (A^H v_b)), A = I (STD2) or M (OPT, Eq. 7)
     prof_count(KC_FWI);
-    k_grad<R><<<blas_blocks(N, 1), 256, 0, st>>>(nb, N, w2_d, (const C*)fb.U, (const C*)fb.V, fb.gext);
+    if (G.stencil == HELM_OPT)
+      k_grad_opt<R><<<blas_blocks(N, 1), 256, 0, st>>>(nb, op->lev[0].nx, op->lev[0].ny, op->lev[0].nz, w2_d,
+                                                      (const C*)fb.U, (const C*)fb.V, fb.gext);
+    else
+      k_grad<R><<<blas_blocks(N, 1), 256, 0, st>>>(nb, N, w2_d, (const C*)fb.U, (const C*)fb.V, fb.gext);
     CKL();
   }
   if (grad) {
@@ -1803,7 +1856,7 @@ helm_op* fwi_op(const helm_grid* grid, const double* m, double omega, const helm
                 int max_rhs, cudaStream_t st) {
   helm_op* o = g_fwi_op;
   auto same = [](const helm_grid& a, const helm_grid& b) {
-    if (a.ndim != b.ndim || a.h != b.h) return false;
+    if (a.ndim != b.ndim || a.h != b.h || a.stencil != b.stencil) return false;
     for (int i = 0; i < 3; ++i)
       if (a.n[i] != b.n[i] || a.pml[i][0] != b.pml[i][0] || a.pml[i][1] != b.pml[i][1]) return false;
     return true;
@@ -1957,6 +2010,10 @@ static helm_status fwi_common(FwiMode mode, const helm_grid* grid, const double*
     if (mode == FW_GN) REQ(out && dm, HELM_ERR_ARG, "output / dm NULL");
     if (mode == FW_JAC) REQ(d_out && dm, HELM_ERR_ARG, "d_out / dm NULL");
     if (mode == FW_FORW) REQ(d_out, HELM_ERR_ARG, "d_out NULL");
+    if (grid->stencil == HELM_OPT)   // the Born source T dm = omega^2 M (u dm) and the off-grid
+                                     // acquisition are implemented for STD2 only (helm.h)
+      REQ(mode != FW_JAC && mode != FW_GN && !acq, HELM_ERR_ARG,
+          "the OPT stencil supports fwi_misfit_grad, fwi_forward and fwi_jacobian_adjoint only");
     const cudaStream_t st = (cudaStream_t)stream;
     helm_op* op = fwi_op(grid, m, 2.0 * M_PI * freq[0], pml, dtype, max_rhs, st);
     helm_solve_opts so = opts ? *opts : default_solve_opts(op);

@@ -21,7 +21,28 @@ template <typename R> struct Geo {
   const cx<R>* dg[3];
   const cx<R>* up[3];
   const cx<R>* zpk;        // packed z coefficients [op][z][lo, dg, up] (ghosts masked, R7)
+  int st;                  // stencil kind: 0 STD2 (D4-D5), 1 OPT (DESIGN R34 2D / R35 3D)
+  int adj;                 // tables are H^H's (D6); OPT: the mass term is then diag(m) M, not M diag(m)
 };
+
+// ----------------------------------------------------------------------------- R34 / R35
+// The paper's higher-order stencils (2D "9pt optimal" [23], 3D "compact 27-pt" [60])
+// as the DESIGN readings define them: product forms of the stretched 1D tables T_a with the
+// averages A = (1/4, 1/2, 1/4) and E = (1/2, 0, 1/2), H = L + omega^2 M diag(m) (Eq. 7 with
+// A = M). Weights: DESIGN R34 / R35 (literal copies; scripts/derive_opt_stencil.py).
+namespace optw {
+constexpr double A9 = 0.58547, C9 = 0.63353, D9 = 0.36647, E9 = 1.0 - C9 - D9;
+constexpr double W1 = 0.36027, W2 = 0.46886, W3 = 0.17087;
+constexpr double M1 = 0.47314, M2 = 0.50415, M3 = 0.02271, M4 = 1.0 - M1 - M2 - M3;
+// 2D: coef(dx, dz) = tx[dx] G9[dz] + tz[dz] G9[dx], G9 = a delta + (1 - a) A
+constexpr double G9_0 = A9 + (1.0 - A9) / 2, G9_1 = (1.0 - A9) / 4;
+// 3D: coef = tx[dx] G27(dy, dz) + ty[dy] G27(dx, dz) + tz[dz] G27(dx, dy),
+// G27 = w1 delta delta + (w2/2)(A delta + delta A) + w3 A A, by number of nonzero offsets
+constexpr double G27_0 = W1 + W2 / 2 + W3 / 4, G27_1 = W2 / 8 + W3 / 8, G27_2 = W3 / 16;
+// mass weight of a neighbour by number of nonzero offsets (2D: centre, edge, corner)
+constexpr double MU9_0 = C9, MU9_1 = D9 / 4, MU9_2 = E9 / 4;
+constexpr double MU27_0 = M1, MU27_1 = M2 / 6, MU27_2 = M3 / 12, MU27_3 = M4 / 8;
+}
 
 // The 1D tables and omega^2 of RHS r's operator.
 template <typename R> struct OpTab {
@@ -396,6 +417,43 @@ __global__ void k_grad(int ns, long long N, const double* __restrict__ w2, const
     for (int s = 0; s < ns; ++s) {
       const double2 u = to_d(U[(long long)s * N + p]), v = to_d(V[(long long)s * N + p]);
       acc += w2[s] * (u.x * v.x + u.y * v.y);
+    }
+    gext[p] += acc;
+  }
+}
+
+// OPT stencils (DESIGN R34 / R35): H = L + omega^2 M diag(m), so T^* z = Re(omega^2 conj(u) (M^H z))
+// (Eqs. 7-8; M real symmetric): g_ext += sum_s Re(omega_s^2 conj(u_s) (M v_s)), the
+// mass distribution gathered per point (ghosts zero, R7), fp64, fixed RHS order.
+template <typename R>
+__global__ void k_grad_opt(int ns, int nx, int ny, int nz, const double* __restrict__ w2, const cx<R>* __restrict__ U,
+                           const cx<R>* __restrict__ V, double* __restrict__ gext) {
+  const long long N = (long long)nx * ny * nz, pl = (long long)nx * ny;
+  const bool d3 = ny > 1;
+  const double mu3[4] = {optw::MU27_0, optw::MU27_1, optw::MU27_2, optw::MU27_3};
+  const double mu2[3] = {optw::MU9_0, optw::MU9_1, optw::MU9_2};
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
+    const int ix = (int)(p % nx), iy = (int)((p / nx) % ny), iz = (int)(p / pl);
+    double acc = 0.0;
+    for (int s = 0; s < ns; ++s) {
+      const cx<R>* v = V + (long long)s * N;
+      double mx = 0.0, my = 0.0;
+      for (int dz = -1; dz <= 1; ++dz) {
+        if (iz + dz < 0 || iz + dz >= nz) continue;
+        for (int dy = d3 ? -1 : 0; dy <= (d3 ? 1 : 0); ++dy) {
+          if (iy + dy < 0 || iy + dy >= ny) continue;
+          for (int dx = -1; dx <= 1; ++dx) {
+            if (ix + dx < 0 || ix + dx >= nx) continue;
+            const int n = (dx != 0) + (dy != 0) + (dz != 0);
+            const double mu = d3 ? mu3[n] : mu2[n];
+            const double2 q = to_d(v[p + dz * pl + dy * nx + dx]);
+            mx += mu * q.x;
+            my += mu * q.y;
+          }
+        }
+      }
+      const double2 u = to_d(U[(long long)s * N + p]);
+      acc += w2[s] * (u.x * mx + u.y * my);
     }
     gext[p] += acc;
   }

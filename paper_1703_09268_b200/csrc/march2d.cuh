@@ -55,7 +55,7 @@ template <typename R, int MODE, int NV> struct MarchShape {
 
 // One march pass over the (strip, z-chunk) items of RHS r owned by warp `wi` of `nw`: the
 // streaming body of k_march2d. Accumulates this warp's partial projections / norms.
-template <typename R, int MODE, int NV, int NVR>
+template <typename R, int MODE, int NV, int NVR, int ST = 0>
 __device__ __forceinline__ void march_pass(const Geo<R>& g, const OpTab<R>& T, const cx<R>* ztr, long long rb0,
                                            const cx<R>* xin, const cx<R>* bin, cx<R>* yout, cx<R>* vout,
                                            const cx<R>* const* Vp, R sc, R cw, const cx<R> (&cv)[(MODE >= 3 && NV > 0) ? NV : 1],
@@ -110,10 +110,15 @@ __device__ __forceinline__ void march_pass(const Geo<R>& g, const OpTab<R>& T, c
       return v;
     };
 
+    auto mval = [&](int sl) -> R { return *reinterpret_cast<const R*>(ring + sl * SB + NX * 32 * sizeof(C) + lane * sizeof(R)); };
+    auto shu = [](C v) { return mkc(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1)); };
+    auto shd = [](C v) { return mkc(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1)); };
+
     // prologue: planes z0-1 .. z0+S-2 into slots 0 .. S-1 (slot of plane q: (q - z0 + 1) % S)
     for (int k = 0; k < S; ++k) issue(z0 - 1 + k, k);
     cpa_wait_n(S - 2);                      // planes z0-1, z0 landed
     C fm = formed(0);
+    R mm = ST == 1 ? mval(0) : (R)0;        // OPT: the model of plane z-1 rides along in a register
     issue(z0 - 1 + S, 0);                   // slot of z0-1 is free again
     C f0 = formed(1);
     int s0 = 1;                             // slot of plane z
@@ -122,15 +127,54 @@ __device__ __forceinline__ void march_pass(const Geo<R>& g, const OpTab<R>& T, c
       cpa_wait_n(S - 2);                    // plane z+1 landed (planes up to z+S-1 issued)
       const C fp = formed(s1);
       // ---- compute plane z
-      const C left = mkc(__shfl_up_sync(0xffffffffu, f0.x, 1), __shfl_up_sync(0xffffffffu, f0.y, 1));
-      const C right = mkc(__shfl_down_sync(0xffffffffu, f0.x, 1), __shfl_down_sync(0xffffffffu, f0.y, 1));
-      const R mz = *reinterpret_cast<const R*>(ring + s0 * SB + NX * 32 * sizeof(C) + lane * sizeof(R));
-      const R wm = T.w2 * mz;
+      const C left = shu(f0), right = shd(f0);
+      const R mz = mval(s0);
       const C lz = ztr[3 * z], dz = ztr[3 * z + 1], uz = ztr[3 * z + 2];
-      C t0 = cmul(mkc(dgx.x + dz.x + wm, dgx.y + dz.y), f0);
-      C t1 = cfma(upx, right, cmul(lox, left));
-      C t2 = cfma(uz, fp, cmul(lz, fm));
-      const C hx = cadd(cadd(t0, t1), t2);
+      C hx;
+      if constexpr (ST == 1) {
+        // R34 (2D "9pt optimal", P:204 [23]): coef(dx, dz) = tx[dx] G9[dz] + tz[dz] G9[dx], and
+        // the mass distribution M (centre C9, edges D9/4, corners E9/4) of m u (Eq. 7, A = M)
+        const R g0 = (R)optw::G9_0, g1 = (R)optw::G9_1;
+        const C ul = shu(fm), ur = shd(fm), dl = shu(fp), dr = shd(fp);   // (x-1, z-1), (x+1, z-1), (x-1, z+1), (x+1, z+1)
+        auto ax = [&](C t, R gz) { return mkc(t.x * gz, t.y * gz); };
+        C acc = cmul(cadd(ax(dgx, g0), ax(dz, g0)), f0);                                  // (0, 0)
+        acc = cfma(cadd(ax(lox, g0), ax(dz, g1)), left, acc);                              // (-1, 0)
+        acc = cfma(cadd(ax(upx, g0), ax(dz, g1)), right, acc);                             // (+1, 0)
+        acc = cfma(cadd(ax(dgx, g1), ax(lz, g0)), fm, acc);                                // (0, -1)
+        acc = cfma(cadd(ax(dgx, g1), ax(uz, g0)), fp, acc);                                // (0, +1)
+        acc = cfma(cadd(ax(lox, g1), ax(lz, g1)), ul, acc);                                // (-1, -1)
+        acc = cfma(cadd(ax(upx, g1), ax(lz, g1)), ur, acc);                                // (+1, -1)
+        acc = cfma(cadd(ax(lox, g1), ax(uz, g1)), dl, acc);                                // (-1, +1)
+        acc = cfma(cadd(ax(upx, g1), ax(uz, g1)), dr, acc);                                // (+1, +1)
+        // forward: M diag(m) u (neighbours' m); adjoint (tables of H^H): diag(m) M u (H^H =
+        // L^H + omega^2 diag(m) M, M real symmetric)
+        const bool adj = g.adj != 0;
+        const R mp = mval(s1);
+        const R mlft = adj ? (R)1 : __shfl_up_sync(0xffffffffu, mz, 1);
+        const R mrgt = adj ? (R)1 : __shfl_down_sync(0xffffffffu, mz, 1);
+        C ms = cscale(f0, (R)optw::MU9_0 * (adj ? (R)1 : mz));
+        ms = cfma(mkc((R)optw::MU9_1 * mlft, (R)0), left, ms);
+        ms = cfma(mkc((R)optw::MU9_1 * mrgt, (R)0), right, ms);
+        ms = cfma(mkc((R)optw::MU9_1 * (adj ? (R)1 : mm), (R)0), fm, ms);
+        ms = cfma(mkc((R)optw::MU9_1 * (adj ? (R)1 : mp), (R)0), fp, ms);
+        if constexpr (optw::MU9_2 != 0.0) {
+          const R mul = adj ? (R)1 : __shfl_up_sync(0xffffffffu, mm, 1), mur = adj ? (R)1 : __shfl_down_sync(0xffffffffu, mm, 1);
+          const R mdl = adj ? (R)1 : __shfl_up_sync(0xffffffffu, mp, 1), mdr = adj ? (R)1 : __shfl_down_sync(0xffffffffu, mp, 1);
+          ms = cfma(mkc((R)optw::MU9_2 * mul, (R)0), ul, ms);
+          ms = cfma(mkc((R)optw::MU9_2 * mur, (R)0), ur, ms);
+          ms = cfma(mkc((R)optw::MU9_2 * mdl, (R)0), dl, ms);
+          ms = cfma(mkc((R)optw::MU9_2 * mdr, (R)0), dr, ms);
+        }
+        const R wm = adj ? T.w2 * mz : T.w2;
+        hx = mkc(acc.x + wm * ms.x, acc.y + wm * ms.y);
+        mm = mz;
+      } else {
+        const R wm = T.w2 * mz;
+        C t0 = cmul(mkc(dgx.x + dz.x + wm, dgx.y + dz.y), f0);
+        C t1 = cfma(upx, right, cmul(lox, left));
+        C t2 = cfma(uz, fp, cmul(lz, fm));
+        hx = cadd(cadd(t0, t1), t2);
+      }
       if (outp) {
         const long long o = xo + (long long)z * nx;
         if constexpr (MODE == 0) {
@@ -184,7 +228,7 @@ __device__ __forceinline__ void form_coeffs(const KCtx& ctx, int r, R& cw, cx<R>
   }
 }
 
-template <typename R, int MODE, int NV>
+template <typename R, int MODE, int NV, int ST = 0>
 __global__ void __launch_bounds__(128)
 k_march2d(const MarchArgs<R> a) {
   pdl_wait();
@@ -234,7 +278,7 @@ k_march2d(const MarchArgs<R> a) {
   // items (strip, z-chunk) of this RHS, strip fastest, dealt round-robin to its warps: warps
   // on neighbouring strips stream the same depth together, so the cache lines shared at
   // strip boundaries are read from HBM once (a balanced contiguous split lost up to 15 %)
-  march_pass<R, MODE, NV, NVR>(g, T, ztr, (long long)r * g.N, a.x, a.b, a.y, a.vout, a.V.p, sc, cw, cv, a.nstrip,
+  march_pass<R, MODE, NV, NVR, ST>(g, T, ztr, (long long)r * g.N, a.x, a.b, a.y, a.vout, a.V.p, sc, cw, cv, a.nstrip,
                                a.nzc, a.zlen, wi, a.wpr, S, ring, ring_s, acc, nrm, ynrm);
 
   if constexpr (MODE != 0) {

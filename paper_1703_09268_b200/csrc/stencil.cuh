@@ -108,10 +108,12 @@ template <typename R> struct PlaneArgs {
   int jskip;
   int jstep;               // Hessenberg column written (MODE 2, 3)
   int nrhs, ntx, nty;      // row tiles: ntx x nty per group (nty = 1 in 2D)
+  int by;                  // tile rows (BY of the launched kernel; host bookkeeping)
   int cpg;                 // CTAs per group
   int nzc, zlen;           // z-chunks per tile and their length
   int S;                   // ring stages (>= 4; split-ring fused steps: raw stages D >= 2)
   int nf;                  // split-ring fused steps: formed slots (3: two barriers per plane, 4: one)
+  int prev;                // single ring: plane z-1 from registers (S-2 planes in flight)
   int tma;                 // TMA stages (tm[0] = x / W, tm[1 + i] = V_i halo'd tiles; tmm = m, tmz = z
                            // coefficients) instead of per-thread cp.async
   CUtensorMap tm[HELM_KMAX + 1];
@@ -121,7 +123,7 @@ template <typename R> struct PlaneArgs {
   RedBuf rb;
 };
 
-template <typename R, int BX, int BY, int NX, int NP, bool YC, bool MREG = false>
+template <typename R, int BX, int BY, int NX, int NP, bool YC, bool MREG = false, bool MH = false>
 struct PlaneSmem {
   static constexpr int YH = YC ? 1 : 0;              // y-halo rows (3D only)
   // TMA boxes must start 16-B aligned along x (measured on B200: an unaligned start faults
@@ -137,10 +139,16 @@ struct PlaneSmem {
   // m is staged in the ring, except for the complex128 five-tile stages (the last Arnoldi
   // steps), where it is register-prefetched two planes ahead so that the stage fits two
   // CTAs per SM (measured: 3.3 -> 4.1 TB/s there; smaller stages are faster with m staged)
-  // (MREG: m always register-prefetched — the split-ring fused steps below)
-  static constexpr bool MR = !MREG && (sizeof(cx<R>) != 16 || NX < 5);
+  // (MREG: m always register-prefetched — the split-ring fused steps below; MH: the OPT
+  // stencils' mass distribution needs m at the 27 neighbours, so m is staged as a halo'd tile,
+  // 16-B aligned box start XOm = 16 B / real before the interior like the complex tiles)
+  static constexpr bool MR = !MREG && (MH || sizeof(cx<R>) != 16 || NX < 5);
+  static constexpr int XOm = (int)(16 / sizeof(R));
+  static constexpr int XPm = BX + 2 * XOm;
+  static constexpr int MEm = (BY + 2 * YH) * XPm;
+  static constexpr size_t m_bytes = MH ? ((size_t)MEm * sizeof(R) + 127) / 128 * 128 : (size_t)PE * sizeof(R);
   static constexpr size_t m_off = (size_t)NX * XS * sizeof(cx<R>);
-  static constexpr size_t p_off = m_off + (MR ? PE * sizeof(R) : 0);
+  static constexpr size_t p_off = m_off + (MR ? m_bytes : 0);
   static constexpr size_t z_off = p_off + (size_t)NP * PE * sizeof(cx<R>);
   static constexpr int ZR = YC ? 1 : BY;               // z-coefficient rows (2D: one per warp)
   static constexpr size_t stage_bytes = (z_off + ZR * 4 * sizeof(cx<R>) + 127) / 128 * 128;
@@ -270,7 +278,40 @@ __device__ inline void plane_epilogue(const KCtx& ctx, int r, int jstep, const d
   }
 }
 
-template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC, bool SPLIT = false>
+// DESIGN R35 (3D "compact 27-pt", P:204 [60]) at one point: L u + omega^2 M (m u) over the
+// 27 neighbours of the halo'd tiles of planes z-1, z, z+1 (X*, complex; M*, the model), from
+// the point's 1D table entries t_a = (lo, dg, up) (ghost entries already zero, R7) and the
+// constant product-form weights (kernels.cuh optw).
+// H^H = L^H + omega^2 diag(m) M (M real symmetric): with adj the mass term is m(centre) times
+// the M-average of u (the tables are already H^H's, D6).
+template <typename R>
+__device__ __forceinline__ cx<R> opt27(const cx<R>* const (&X)[3], const R* const (&Mh)[3], int c, int cm, int XP,
+                                       int XPm, const cx<R> (&tx)[3], const cx<R> (&ty)[3], const cx<R> (&tz)[3],
+                                       R w2, bool adj) {
+  using C = cx<R>;
+  constexpr R G[3] = {(R)optw::G27_0, (R)optw::G27_1, (R)optw::G27_2};
+  constexpr R MU[4] = {(R)optw::MU27_0, (R)optw::MU27_1, (R)optw::MU27_2, (R)optw::MU27_3};
+  C acc = mkc((R)0, (R)0), ms = mkc((R)0, (R)0);
+#pragma unroll
+  for (int iz = 0; iz < 3; ++iz)
+#pragma unroll
+    for (int iy = 0; iy < 3; ++iy)
+#pragma unroll
+      for (int ix = 0; ix < 3; ++ix) {
+        const int nx_ = ix != 1, ny_ = iy != 1, nz_ = iz != 1;
+        const C u = X[iz][c + (iy - 1) * XP + (ix - 1)];
+        // coefficient: tx[ix] G(dy, dz) + ty[iy] G(dx, dz) + tz[iz] G(dx, dy)
+        const R gx = G[ny_ + nz_], gy = G[nx_ + nz_], gz = G[nx_ + ny_];
+        const C cf = mkc(tx[ix].x * gx + ty[iy].x * gy + tz[iz].x * gz, tx[ix].y * gx + ty[iy].y * gy + tz[iz].y * gz);
+        acc = cfma(cf, u, acc);
+        const R mu = MU[nx_ + ny_ + nz_];
+        if (mu != (R)0) ms = cfma(mkc(adj ? mu : mu * Mh[iz][cm + (iy - 1) * XPm + (ix - 1)], (R)0), u, ms);
+      }
+  const R wm = adj ? w2 * Mh[1][cm] : w2;
+  return mkc(acc.x + wm * ms.x, acc.y + wm * ms.y);
+}
+
+template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC, bool SPLIT = false, int ST = 0>
 __global__ void __launch_bounds__(BX * BY / PY)
 k_plane(const __grid_constant__ PlaneArgs<R> a) {
   pdl_wait();
@@ -278,9 +319,10 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
   using C = cx<R>;
   using Sh = PlaneShape<MODE, NV>;
   constexpr int NX = Sh::NX, NP = Sh::NP, NVR = Sh::NVR;
-  using SM = PlaneSmem<R, BX, BY, NX, NP, YC, SPLIT>;
+  using SM = PlaneSmem<R, BX, BY, NX, NP, YC, SPLIT, ST == 1>;
   using FS = FormSlot<R, BX, BY, YC>;
   static_assert(!SPLIT || (MODE >= 3 && NV > 0 && YC), "split ring: fused GMRES steps that form v_NV (3D)");
+  static_assert(!(SPLIT && ST == 1), "the OPT stencil runs on the single ring");
   constexpr int YH = SM::YH;
   constexpr int NT = BX * BY / PY;
   constexpr int RS = BY / PY;          // row stride between a thread's rows
@@ -415,14 +457,17 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
             const unsigned bar = mbase + 8 * stg;
             // full boxes (OOB zero-filled): the halo'd tiles, m's own points, the z row
             mbar_expect_tx(bar, (unsigned)(NX * SM::XE * sizeof(C) +
-                                           (tmq ? (SM::MR ? SM::PE * sizeof(R) : 0) + 4 * sizeof(C) : 0)));
+                                           (tmq ? (SM::MR ? (ST == 1 ? SM::MEm : SM::PE) * sizeof(R) : 0) +
+                                                      4 * sizeof(C)
+                                                : 0)));
             constexpr int CR = (int)(sizeof(C) / 8);   // tensor element = one 8-byte word
 #pragma unroll
             for (int t = 0; t < NX; ++t)
               tma_load4(st + (unsigned)(t * SM::XS * sizeof(C)), &a.tm[t], bar, CR * (txb * BX - XO), tyb * BY - YH, z,
                         rhs[0]);
             if (tmq) {
-              if constexpr (SM::MR) tma_load3(st + (unsigned)SM::m_off, &a.tmm, bar, txb * BX, tyb * BY, z);
+              if constexpr (ST == 1) tma_load3(st + (unsigned)SM::m_off, &a.tmm, bar, txb * BX - SM::XOm, tyb * BY - 1, z);
+              else if constexpr (SM::MR) tma_load3(st + (unsigned)SM::m_off, &a.tmm, bar, txb * BX, tyb * BY, z);
               tma_load2(st + (unsigned)SM::z_off, &a.tmz, bar, 0, zrow0 + z);
             }
           }
@@ -450,7 +495,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           for (int k = 0; k < PY; ++k)
             if (rok[k]) {
               const int pr = (ty0 + k * RS) * BX + tx;
-              if constexpr (SM::MR)
+              if constexpr (SM::MR && ST == 0)
                 if (!tmq)
                   cpa<sizeof(R)>(st + (unsigned)(SM::m_off + pr * sizeof(R)), g.m + (YC ? mofs0 + (long long)k * RS * nx : mofs0) + zo, true);
               if constexpr (MODE == 1) cpa<sizeof(C)>(st + (unsigned)(SM::p_off + pr * sizeof(C)), a.b + gofs[k] + zo, true);
@@ -514,9 +559,15 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
     // plane being formed (vn), captured from the raw stage before it is refilled
     constexpr int NVD = SPLIT ? NV : 1;
     C vd[PY][NVD], vn[PY][NVD];
+    // single ring, STD2: plane z-1 enters only through the own-point z-neighbour term, so each
+    // thread keeps it in registers (prevc) and its stage is refilled one plane earlier
+    constexpr bool PREV_OK = !SPLIT && ST == 0;
+    const bool PREV = PREV_OK && a.prev != 0;   // HELM_PREV=0: the round-1 ring (A/B)
+    C prevc[PY];
     // plane z from the tiles of planes z-1, z, z+1 (X0, X1, X2; x/y halo in X1), m (Ms or
     // registers), the own-point operands (Ps) and the plane's z coefficients (Zt)
-    auto compute = [&](int z, const C* X0, const C* X1, const C* X2, const R* Ms, const C* Ps, const C* Zt) {
+    auto compute = [&](int z, const C* X0, const C* X1, const C* X2, const R* Ms, const C* Ps, const C* Zt,
+                       const R* Ms0 = nullptr, const R* Ms2 = nullptr) {
       const C lz = Zt[(YC ? 0 : ty0) * 4], dz = Zt[(YC ? 0 : ty0) * 4 + 1], uz = Zt[(YC ? 0 : ty0) * 4 + 2];
       const long long zo = (long long)z * plane;
 #pragma unroll
@@ -525,13 +576,23 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
         const int c = (ty0 + k * RS + YH) * XP + tx + XO;
         const int pr = (ty0 + k * RS) * BX + tx;
         const C cur = X1[c];
-        const R wm = T.w2 * (SM::MR ? Ms[pr] : mr0[k]);
-        // tree-shaped sum: four independent complex products, then two adds
-        C t0 = cmul(mkc(dgx.x + dgy[k].x + dz.x + wm, dgx.y + dgy[k].y + dz.y), cur);
-        C t1 = cfma(upx, X1[c + 1], cmul(lox, X1[c - 1]));
-        C t2 = cfma(uz, X2[c], cmul(lz, X0[c]));
-        if constexpr (YC) t0 = cfma(upy[k], X1[c + XP], cfma(loy[k], X1[c - XP], t0));
-        const C hx = cadd(cadd(t0, t1), t2);
+        C hx;
+        if constexpr (ST == 1) {   // R35: the 27-point stencil with the mass distribution
+          const int cm = (ty0 + k * RS + YH) * SM::XPm + tx + SM::XOm;
+          const C* const Xs[3] = {X0, X1, X2};
+          const R* const Mh[3] = {Ms0, Ms, Ms2};
+          const C txa[3] = {lox, dgx, upx}, tya[3] = {loy[k], dgy[k], upy[k]}, tza[3] = {lz, dz, uz};
+          hx = opt27<R>(Xs, Mh, c, cm, XP, SM::XPm, txa, tya, tza, T.w2, g.adj != 0);
+        } else {
+          const R wm = T.w2 * (SM::MR ? Ms[pr] : mr0[k]);
+          // tree-shaped sum: four independent complex products, then two adds
+          C t0 = cmul(mkc(dgx.x + dgy[k].x + dz.x + wm, dgx.y + dgy[k].y + dz.y), cur);
+          C t1 = cfma(upx, X1[c + 1], cmul(lox, X1[c - 1]));
+          C t2 = cfma(uz, X2[c], cmul(lz, PREV ? prevc[k] : X0[c]));
+          if constexpr (YC) t0 = cfma(upy[k], X1[c + XP], cfma(loy[k], X1[c - XP], t0));
+          hx = cadd(cadd(t0, t1), t2);
+        }
+        if constexpr (PREV_OK) prevc[k] = cur;   // plane z is the next plane's z-1
         C* yp = a.y + gofs[k] + zo;
         if constexpr (MODE == 0) {
           *yp = cscale(hx, sc);
@@ -628,6 +689,49 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
 #pragma unroll
           for (int v = 0; v < NV; ++v) vd[k][v] = vn[k][v];
       }
+    } else if (PREV) {
+      // ---- single ring, plane z-1 in registers: the stage of plane q is q % S; at plane z the
+      // stage of z-1 is free, so S-2 planes are in flight (the ncu stall profile of the fused
+      // steps at cfg4 level 1 showed 20 % of warp time waiting for TMA stages with S-3 = 1)
+      auto inc = [S](int x) { return x + 1 == S ? 0 : x + 1; };
+      for (int q = 0; q < S; ++q) load(q, q);      // planes z0-1 .. z0+S-2
+      if (cpa_on) cpa_wait_n(S - 1);               // plane z0-1 (this thread's copies)
+      if (tma) mbar_wait(mbase, (pbits & 1u) ^ 1u);
+      csync<YC>();
+      if constexpr (FORM) {
+        form(0);
+        csync<YC>();
+      }
+      {
+        const C* Xm = reinterpret_cast<const C*>(smem);
+#pragma unroll
+        for (int k = 0; k < PY; ++k) prevc[k] = rok[k] ? Xm[(ty0 + k * RS + YH) * XP + tx + XO] : zero;
+      }
+      if constexpr (!SM::MR) { ldm(z0, mr0); ldm(z0 + 1, mr1); }
+      int s_fr = 0, s_0 = 1, s_p1 = 2;             // stages of planes z-1 (free), z, z+1
+      for (int z = z0; z < z1; ++z) {
+        const int q = z - z0 + 1;
+        if (cpa_on) cpa_wait_n(S - 3);   // this thread's groups <= q+1 complete (committed: <= q+S-2)
+        if (tma) {
+          if (z == z0) mbar_wait(mbase + 8 * s_0, ((pbits >> s_0) & 1u) ^ 1u);
+          mbar_wait(mbase + 8 * s_p1, ((pbits >> s_p1) & 1u) ^ 1u);
+        }
+        csync<YC>();                     // every thread is done with plane z-1: its stage is free
+        load(q + S - 1, s_fr);           // S-2 planes in flight while plane z is computed
+        if constexpr (FORM) {
+          if (z == z0) form(s_0);
+          form(s_p1);
+          csync<YC>();
+        }
+        const unsigned char* st1 = smem + s_0 * SM::stage_bytes;
+        if constexpr (!SM::MR) ldm(z + 2, mr2);
+        compute(z, nullptr, reinterpret_cast<const C*>(st1), reinterpret_cast<const C*>(smem + s_p1 * SM::stage_bytes),
+                reinterpret_cast<const R*>(st1 + SM::m_off), reinterpret_cast<const C*>(st1 + SM::p_off),
+                reinterpret_cast<const C*>(st1 + SM::z_off));
+        s_fr = s_0;
+        s_0 = s_p1;
+        s_p1 = inc(s_p1);
+      }
     } else {
       // ring stages are tracked incrementally (no division on the streaming path)
       auto inc = [S](int x) { return x + 1 == S ? 0 : x + 1; };
@@ -659,7 +763,9 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
         if constexpr (!SM::MR) ldm(z + 2, mr2);
         compute(z, reinterpret_cast<const C*>(smem + s_m1 * SM::stage_bytes), reinterpret_cast<const C*>(st1),
                 reinterpret_cast<const C*>(smem + s_p1 * SM::stage_bytes), reinterpret_cast<const R*>(st1 + SM::m_off),
-                reinterpret_cast<const C*>(st1 + SM::p_off), reinterpret_cast<const C*>(st1 + SM::z_off));
+                reinterpret_cast<const C*>(st1 + SM::p_off), reinterpret_cast<const C*>(st1 + SM::z_off),
+                reinterpret_cast<const R*>(smem + s_m1 * SM::stage_bytes + SM::m_off),
+                reinterpret_cast<const R*>(smem + s_p1 * SM::stage_bytes + SM::m_off));
         s_m1 = s_0;
       }
     }

@@ -19,8 +19,8 @@ HBM = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspat
     if os.path.exists(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) else 6650.0
 
 
-def run(N, dt, b, adjoint=0, reps=10):
-    p = synth.cfg5(N)
+def run(N, dt, b, adjoint=0, reps=10, stencil="std2"):
+    p = synth.cfg5(N).with_(stencil=stencil)
     dtype = api.C128 if dt == "c128" else api.C64
     op = api.helm_setup(api.Grid.of(p), p.m, 2 * np.pi * 6.0, api.Pml(v_ref=4500.0), dtype, max_rhs=b,
                         mlopts=api.MlOpts(levels=0))
@@ -44,7 +44,7 @@ def run(N, dt, b, adjoint=0, reps=10):
         ts.append(e0.elapsed_time(e1) / 1e3)
     t = statistics.median(ts)
     bytes_ = p.n_ext * (2 * sc * b + sr)
-    out = {"N": N, "dtype": dt, "b": b, "adjoint": adjoint, "ms_median": t * 1e3, "ms_best": min(ts) * 1e3,
+    out = {"N": N, "dtype": dt, "b": b, "adjoint": adjoint, "stencil": stencil, "ms_median": t * 1e3, "ms_best": min(ts) * 1e3,
            "gpts": p.n_ext * b / t / 1e9, "GBps": bytes_ / t / 1e9, "frac_measured": bytes_ / t / 1e9 / HBM,
            "frac_8TBs": bytes_ / t / 8e12, "alg_bytes": bytes_}
     del xs, ys, op
@@ -57,10 +57,11 @@ if __name__ == "__main__":
     ap.add_argument("--N", default="128,256,384,512")
     ap.add_argument("--dtype", default="c128,c64")
     ap.add_argument("--b", default="1,4,16")
+    ap.add_argument("--stencil", default="std2")
     a = ap.parse_args()
     for N in [int(v) for v in a.N.split(",")]:
         for dt in a.dtype.split(","):
             for b in [int(v) for v in a.b.split(",")]:
                 if N == 512 and b == 16 and dt == "c128":
                     pass
-                print(json.dumps(run(N, dt, b)), flush=True)
+                print(json.dumps(run(N, dt, b, stencil=a.stencil)), flush=True)

@@ -47,15 +47,16 @@ def test_bad_arguments_fail_before_any_device_work():
 def test_ctypes_layout_matches_c(tmp_path):
     prog = tmp_path / "sz.c"
     prog.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "helm.h"\nint main(){'
-                    'printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(helm_grid), offsetof(helm_grid,h),'
+                    'printf("%zu %zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(helm_grid), offsetof(helm_grid,h),'
                     'offsetof(helm_grid,pml), sizeof(helm_pml), sizeof(helm_mlopts), sizeof(helm_solve_opts),'
-                    'sizeof(helm_solve_report), offsetof(helm_solve_report,bytes_alg)); return 0;}')
+                    'sizeof(helm_solve_report), offsetof(helm_solve_report,bytes_alg), offsetof(helm_grid,stencil));'
+                    ' return 0;}')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)])
     got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
     want = [ctypes.sizeof(_lib.HelmGrid), _lib.HelmGrid.h.offset, _lib.HelmGrid.pml.offset,
             ctypes.sizeof(_lib.HelmPml), ctypes.sizeof(_lib.HelmMlOpts), ctypes.sizeof(_lib.HelmSolveOpts),
-            ctypes.sizeof(_lib.HelmSolveReport), _lib.HelmSolveReport.bytes_alg.offset]
+            ctypes.sizeof(_lib.HelmSolveReport), _lib.HelmSolveReport.bytes_alg.offset, _lib.HelmGrid.stencil.offset]
     assert got == want
 
 
