@@ -519,8 +519,12 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
   a.cpg = sp.cpg; a.nzc = sp.nzc; a.zlen = sp.zlen;
   a.S = cfg.S;
   a.nf = cfg.nf;
-  static const int prev_on = env_int("HELM_PREV", 1);
-  a.prev = prev_on;
+  // plane z-1 in registers (stencil.cuh PREV): same-box A/B (profiles/r02/probe_prev_ab.txt) at
+  // cfg4: residual and fused steps at level 1 +7-19 %, level-0 residual +23 %, level-0 steps
+  // 1-2 -7 %; the cfg5 matvec (MODE 0) lost 3-13 %, so MODE 0 keeps the round-1 ring.
+  // HELM_PREV: 1 (default) modes 1-4, 2 every mode, 0 none.
+  static const int prev_mode = env_int("HELM_PREV", 1);
+  a.prev = prev_mode == 2 || (prev_mode == 1 && MODE != 0);
   if (env_int("HELM_DEBUG", 0) > 1)
     std::fprintf(stderr, "[helm] plane launch mode=%d nv=%d split=%d groups=%d cpg=%d nzc=%d zlen=%d tiles=%d\n", MODE, NV,
                  (int)SPLIT, groups, sp.cpg, sp.nzc, sp.zlen, a.ntx * a.nty);

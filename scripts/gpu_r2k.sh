@@ -1,0 +1,25 @@
+# Round 2, call K: the closing evidence — path parity, the full default bench line (driver's
+# K/W), the bench command's ncu launch list, ncu --set full of the level-1 fused steps.
+set -x
+mkdir -p gpurun_out
+T=r2k
+timeout 900 python -m pytest tests/test_gpu_paths.py tests/test_gpu_solve.py -q -m gpu > gpurun_out/${T}_tests.log 2>&1
+echo "tests rc=$?"
+python bench.py --steps 20 --warmup 5 > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
+echo "bench rc=$?"
+CMD="python bench.py --steps 1 --warmup 3 --no-matvec --no-cpu-baseline --no-extra"
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -s 120000 -c 2000 --csv \
+    --log-file gpurun_out/${T}_bench_launches.csv $CMD > gpurun_out/${T}_ncu_launches.log 2>&1
+echo "launch list rc=$?"
+for spec in "3 0" "3 1" "3 2" "3 3" "4 4"; do
+  set -- $spec
+  name=${T}_cfg4_L1_k$1_nv$2
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_plane -s 2 -c 1 \
+      -o gpurun_out/${name} python scripts/ncu_targets.py probe cfg4_8 1 $1 $2 > gpurun_out/${name}_ncu.log 2>&1
+  echo "$name rc=$?"
+  if [ -f gpurun_out/${name}.ncu-rep ]; then
+    ncu -i gpurun_out/${name}.ncu-rep --page raw --csv > gpurun_out/${name}_raw.csv 2>/dev/null
+    ncu -i gpurun_out/${name}.ncu-rep --page details > gpurun_out/${name}_details.txt 2>/dev/null
+    rm -f gpurun_out/${name}.ncu-rep
+  fi
+done

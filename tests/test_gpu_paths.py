@@ -7,7 +7,8 @@ plane, HELM_SPLIT_OCC=4) or two raw stages (HELM_SPLIT_D=2), and coarse V-cycles
 one grid-synchronous launch instead of a launch sequence (HELM_PERSIST=1; the level-1
 V-cycle is also compared with the numpy mirror, <= 1e-12, and must take <= 2 launches), and
 32 x 16 matvec tiles (HELM_MATVEC_BY=16), and the round-1 single ring that keeps plane z-1 in
-shared memory (HELM_PREV=0). Each must match the assembled oracle H (c128 <= 1e-12, c64 <= 1e-5) for
+shared memory (HELM_PREV=0) or keeps it in registers in every mode including the matvec
+(HELM_PREV=2). Each must match the assembled oracle H (c128 <= 1e-12, c64 <= 1e-5) for
 helm_apply forward / adjoint on a ragged multi-tile grid, and give a certified solve."""
 import json
 import os
@@ -68,9 +69,10 @@ print(json.dumps(out))
 
 @pytest.mark.parametrize("env", [{"HELM_TMA": "0"}, {"HELM_TMA_MZ": "0"}, {"HELM_PLANE_PY": "2"},
                                  {"HELM_SPLIT": "0"}, {"HELM_SPLIT": "2"}, {"HELM_SPLIT": "2", "HELM_SPLIT_OCC": "4"},
-                                 {"HELM_SPLIT": "2", "HELM_SPLIT_D": "2"}, {"HELM_PERSIST": "1"}, {"HELM_MATVEC_BY": "16"}, {"HELM_PREV": "0"}],
+                                 {"HELM_SPLIT": "2", "HELM_SPLIT_D": "2"}, {"HELM_PERSIST": "1"}, {"HELM_MATVEC_BY": "16"}, {"HELM_PREV": "0"}, {"HELM_PREV": "2"}],
                          ids=["cpasync", "tma_tiles_only", "py2", "single_ring", "split_all", "split_nf3", "split_d2",
-                              "persistent_vcycle", "matvec_by16", "ring_without_register_plane"])
+                              "persistent_vcycle", "matvec_by16", "ring_without_register_plane",
+                              "register_plane_every_mode"])
 def test_alternative_stage_paths_match_oracle(env):
     e = dict(os.environ, PYTHONPATH=ROOT + os.pathsep + os.environ.get("PYTHONPATH", ""), **env)
     r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
