@@ -117,13 +117,18 @@ helm_status helm_setup(const helm_grid* grid, const double* m_slowness2, double 
 
 /* a2 (Eq. 1). y = H x (adjoint = 0) or y = H^H x (adjoint = 1) for
  * nrhs right-hand sides on the finest extended grid; x, y device, dtype of the op, must not
- * alias. H = sum_a T_a + omega^2 diag(E m) (D5), zero Dirichlet ghosts (R7). */
+ * alias. H = sum_a T_a + omega^2 diag(E m) (D5; grid.stencil = HELM_OPT: R34 / R35),
+ * zero Dirichlet ghosts (R7). Asynchronous on cuda_stream. */
 helm_status helm_apply(helm_op* op, int32_t adjoint, int32_t nrhs, const void* x_dev,
                        void* y_dev, void* cuda_stream);
 
 /* a3-a6 (+a8 with adjoint = 1). Solves H x = b (or H^H x = b) for nrhs independent RHS
- * (R27) with FGMRES(k_inner) + ML-GMRES. b_dev, x_dev: device, extended grid, dtype of the
- * op; x_dev is output only (x0 = 0). report_host: NULL or an array of nrhs reports. */
+ * (R27) with the paper's solver: outer FGMRES with k_inner = 5 inner iterations to a true
+ * relative residual of rtol = 1e-6 (R23), right-preconditioned by the ML-GMRES cycle
+ * of §5 (Alg. 1, recursion Fig. 3; counts (3,5,3,5) P:284; GMRES
+ * smoothers P:274). b_dev, x_dev: device, extended grid, dtype of the op; x_dev is output
+ * only (x0 = 0). report_host: NULL or an array of nrhs reports. Returns after
+ * completion. Non-convergence within max_outer is not an error (converged = 0). */
 helm_status helm_solve(helm_op* op, int32_t adjoint, int32_t nrhs, const void* b_dev,
                        void* x_dev, const helm_solve_opts* opts,
                        helm_solve_report* report_host, void* cuda_stream);

@@ -515,7 +515,13 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
     return c;
   }();
   ensure_smem_optin(kern);   // this device (the cached configuration may come from another one)
-  const PlaneSplit sp = plane_split(groups, (long long)num_sms() * cfg.occ, a.ntx * a.nty, a.g.nz);
+  PlaneSplit sp = plane_split(groups, (long long)num_sms() * cfg.occ, a.ntx * a.nty, a.g.nz);
+  static const int nzc_fix = env_int("HELM_PLANE_NZC", 0);   // tuning: force the z-chunk count
+  if (nzc_fix > 0) {
+    sp.zlen = (a.g.nz + nzc_fix - 1) / nzc_fix;
+    sp.nzc = (a.g.nz + sp.zlen - 1) / sp.zlen;
+    sp.cpg = (int)std::min<long long>(std::max(1LL, (long long)num_sms() * cfg.occ / groups), (long long)a.ntx * a.nty * sp.nzc);
+  }
   a.cpg = sp.cpg; a.nzc = sp.nzc; a.zlen = sp.zlen;
   a.S = cfg.S;
   a.nf = cfg.nf;

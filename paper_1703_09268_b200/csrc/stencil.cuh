@@ -716,13 +716,15 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           if (z == z0) mbar_wait(mbase + 8 * s_0, ((pbits >> s_0) & 1u) ^ 1u);
           mbar_wait(mbase + 8 * s_p1, ((pbits >> s_p1) & 1u) ^ 1u);
         }
-        csync<YC>();                     // every thread is done with plane z-1: its stage is free
-        load(q + S - 1, s_fr);           // S-2 planes in flight while plane z is computed
+        // forming needs no barrier before it: v_NV of plane z+1 goes into tile 0 of its own
+        // (landed) stage, which no thread still in plane z-1 reads; the one barrier below both
+        // publishes it and frees the stage of plane z-1 (every thread is past plane z-1)
         if constexpr (FORM) {
           if (z == z0) form(s_0);
           form(s_p1);
-          csync<YC>();
         }
+        csync<YC>();
+        load(q + S - 1, s_fr);           // S-2 planes in flight while plane z is computed
         const unsigned char* st1 = smem + s_0 * SM::stage_bytes;
         if constexpr (!SM::MR) ldm(z + 2, mr2);
         compute(z, nullptr, reinterpret_cast<const C*>(st1), reinterpret_cast<const C*>(smem + s_p1 * SM::stage_bytes),

@@ -23,9 +23,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--max-rhs", type=int, default=16)
 ap.add_argument("--dtype", default="c128")
 ap.add_argument("--n", type=int, default=200)
+ap.add_argument("--nsrc", type=int, default=64)
 a = ap.parse_args()
 t0 = time.perf_counter()
 p = synth.cfg4(n=a.n)
+p = p.with_(src=p.src[:a.nsrc])
 grid = api.Grid.of(p)
 pml = api.Pml(v_ref=4500.0)
 dt = api.C64 if a.dtype == "c64" else api.C128
@@ -48,7 +50,8 @@ levels = {}
 for lv in range(4):
     pr = api.profile_read(lv)
     row = {k: {"est_ms": round(v["ms"] * v["launches"] / v["sampled"], 1),
-               "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)} for k, v in pr.items() if v["sampled"]}
+               "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1), "launches": v["launches"],
+               "us_per_launch": round(1e3 * v["ms"] / v["sampled"], 1)} for k, v in pr.items() if v["sampled"]}
     if row:
         levels[lv] = row
 api.profile(False, 1)
