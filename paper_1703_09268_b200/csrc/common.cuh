@@ -55,6 +55,9 @@ struct KCtx {
   int* kact;       // [nrhs]          active Krylov dimension (breakdown / zero rhs)
   double2* y;      // [nrhs][KMAX]    least-squares solution R y = g of the cycle (set when
                    //                 its last column closes; zero until then)
+  double2* fc;     // [nrhs][KMAX+1]  forming coefficients of the last basis vector of the cycle,
+                   //                 V_{k-1} = fc_{k-1} W + sum_{i<k-1} fc_i V_i (saved by the
+                   //                 last fused step, which does not store V_{k-1}, 3D)
   int k;           // inner dimension of this process
 };
 

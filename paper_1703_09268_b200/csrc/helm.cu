@@ -247,6 +247,7 @@ KCtx make_ctx(std::vector<void*>& keep, int nrhs, int k) {
   c.g = dalloc<double2>(keep, (size_t)nrhs * K1);
   c.kact = dalloc<int>(keep, nrhs);
   c.y = dalloc<double2>(keep, (size_t)nrhs * HELM_KMAX);
+  c.fc = dalloc<double2>(keep, (size_t)nrhs * K1);
   CK(cudaMemset(c.y, 0, sizeof(double2) * nrhs * HELM_KMAX));
   c.k = k;
   CK(cudaMemset(c.H, 0, sizeof(double2) * nrhs * K1 * HELM_KMAX));
@@ -452,7 +453,7 @@ struct PlaneCfg { int S = 0, occ = 0, nf = 0; size_t smem = 0; };
 // Split of a group's T tiles x nz planes over its CTAs (one resident wave of G CTAs over
 // all groups): the z-chunk count minimising waves x (chunk planes + 2 halo planes).
 struct PlaneSplit { int cpg, nzc, zlen; };
-PlaneSplit plane_split(int groups, long long G, int T, int nz) {
+PlaneSplit plane_split(int groups, long long G, int T, int nz, int hw10 = 20) {
   const long long cpg0 = std::max(1LL, G / groups);
   long long best = -1;
   PlaneSplit r{1, 1, nz};
@@ -461,7 +462,7 @@ PlaneSplit plane_split(int groups, long long G, int T, int nz) {
     if (nzc != n) continue;
     const long long items = (long long)T * nzc;
     const long long waves = (items + cpg0 - 1) / cpg0;
-    const long long cost = waves * (zl + 2);
+    const long long cost = waves * (10LL * zl + hw10);   // hw10: per-item overhead in tenths of a plane
     if (best < 0 || cost < best) { best = cost; r = PlaneSplit{(int)std::min(cpg0, items), nzc, zl}; }
   }
   return r;
@@ -482,7 +483,9 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
   using Sh = PlaneShape<MODE, NV>;
   constexpr int NT = 32 * BY / PY;
   constexpr size_t sb = PlaneSmem<R, 32, BY, Sh::NX, Sh::NP, YC, SPLIT, ST == 1>::stage_bytes;
-  auto kern = k_plane<R, 32, BY, PY, MODE, NV, YC, SPLIT, ST>;
+  void (*kern)(PlaneArgs<R>) = nullptr;
+  if constexpr (PY == 1 && MODE >= 3 && ST == 0) kern = k_plane_o2<R, 32, BY, PY, MODE, NV, YC, SPLIT, ST>;
+  else kern = k_plane<R, 32, BY, PY, MODE, NV, YC, SPLIT, ST>;
   static const PlaneCfg cfg = [&] {
     PlaneCfg c;
     const PlaneTune& t = plane_tune<R, PY>();
@@ -515,7 +518,21 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
     return c;
   }();
   ensure_smem_optin(kern);   // this device (the cached configuration may come from another one)
-  PlaneSplit sp = plane_split(groups, (long long)num_sms() * cfg.occ, a.ntx * a.nty, a.g.nz);
+  // plane z-1 in registers (stencil.cuh PREV): same-box A/B (profiles/r02/probe_prev_ab.txt) at
+  // cfg4: residual and fused steps at level 1 +7-19 %, level-0 residual +23 %, level-0 steps
+  // 1-2 -7 %; the cfg5 matvec (MODE 0) lost 3-13 %, so MODE 0 keeps the round-1 ring.
+  // HELM_PREV: 1 (default) modes 1-4, 2 every mode, 0 none.
+  static const int prev_mode = env_int("HELM_PREV", 1);
+  a.prev = prev_mode == 2 || (prev_mode == 1 && MODE != 0);
+  // continuous ring across a CTA's items (fused steps with TMA-only stages; HELM_CONT=0: per-item
+  // ring fills, the round-2 kernel). An item then costs its planes plus the two halo planes'
+  // loads and forming, not a ring refill: HELM_CONT_HW10 = that overhead in tenths of a plane.
+  static const int cont_on = env_int("HELM_CONT", 1);
+  static const int cont_hw10 = env_int("HELM_CONT_HW10", 10);
+  static const int ctared = env_int("HELM_CTA_RED", 1);   // CTA-level reduction tail (stencil.cuh)
+  a.ctared = ctared;
+  a.cont = (MODE >= 3 && !SPLIT && ST == 0 && cont_on && a.tma && a.tmq && a.prev) ? 1 : 0;
+  PlaneSplit sp = plane_split(groups, (long long)num_sms() * cfg.occ, a.ntx * a.nty, a.g.nz, a.cont ? cont_hw10 : 20);
   static const int nzc_fix = env_int("HELM_PLANE_NZC", 0);   // tuning: force the z-chunk count
   if (nzc_fix > 0) {
     sp.zlen = (a.g.nz + nzc_fix - 1) / nzc_fix;
@@ -525,15 +542,9 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
   a.cpg = sp.cpg; a.nzc = sp.nzc; a.zlen = sp.zlen;
   a.S = cfg.S;
   a.nf = cfg.nf;
-  // plane z-1 in registers (stencil.cuh PREV): same-box A/B (profiles/r02/probe_prev_ab.txt) at
-  // cfg4: residual and fused steps at level 1 +7-19 %, level-0 residual +23 %, level-0 steps
-  // 1-2 -7 %; the cfg5 matvec (MODE 0) lost 3-13 %, so MODE 0 keeps the round-1 ring.
-  // HELM_PREV: 1 (default) modes 1-4, 2 every mode, 0 none.
-  static const int prev_mode = env_int("HELM_PREV", 1);
-  a.prev = prev_mode == 2 || (prev_mode == 1 && MODE != 0);
   if (env_int("HELM_DEBUG", 0) > 1)
-    std::fprintf(stderr, "[helm] plane launch mode=%d nv=%d split=%d groups=%d cpg=%d nzc=%d zlen=%d tiles=%d\n", MODE, NV,
-                 (int)SPLIT, groups, sp.cpg, sp.nzc, sp.zlen, a.ntx * a.nty);
+    std::fprintf(stderr, "[helm] plane launch mode=%d nv=%d split=%d cont=%d groups=%d cpg=%d nzc=%d zlen=%d tiles=%d\n", MODE,
+                 NV, (int)SPLIT, a.cont, groups, sp.cpg, sp.nzc, sp.zlen, a.ntx * a.nty);
   const long long cpg = sp.cpg;
   pdl_launch(kern, dim3((unsigned)(groups * cpg)), dim3(NT), cfg.smem, st, a);
 }
@@ -621,6 +632,15 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
 // 2: y = s H x with the fused projections h_ij = <V_i, y>, i < nv (nv = j + 1);
 // 3: fused Arnoldi step nv of unpreconditioned GMRES (x = raw W or V_0, V = basis, vout);
 // 4: its last step (Y not stored, the last column finalised by Pythagoras).
+// Does the last fused Arnoldi step of a GMRES cycle store V_{k-1}? 2D (march kernel): yes.
+// 3D: no (HELM_LASTV=1: yes, the round-2 schedule) — the solution update reforms it from
+// W = Y_{k-2} and V_0..V_{k-2} with the forming coefficients the step's epilogue saves
+// (KCtx::fc), one vector write less per restart cycle.
+bool last_v_stored(const helm_op* op, int l) {
+  static const bool lastv = env_int("HELM_LASTV", 0) != 0;
+  return lastv || op->lev[l].ny == 1;
+}
+
 template <typename R>
 void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* x, cx<R>* y, const cx<R>* b,
                   const VPtrs<R>* V, int nv, const double* xscale, const int* kact, int j, const KCtx& ctx,
@@ -633,7 +653,7 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
   else if (mode == 1) per = 3 * Sc + Sr;
   else if (mode == 2) per = (2 + nv) * Sc + Sr;
   else if (mode == 3) per = (nv == 0 ? 2 : nv + 3) * Sc + Sr;
-  else per = (nv == 0 ? 1 : nv + 2) * Sc + Sr;   // last step: Y is not stored
+  else per = (nv == 0 ? 1 : nv + (last_v_stored(op, l) ? 2 : 1)) * Sc + Sr;   // last step: Y (3D: nor V_nv) not stored
   if (op->lev[l].ny == 1) {   // 2D: register z-march
     MarchArgs<R> m{};
     m.g = geo<R>(op, l, adj);
@@ -666,6 +686,7 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
   a.xscale = xscale; a.sstride = K1; a.active = op->active_d; a.kact = kact; a.jstep = j;
   a.jskip = mode >= 3 ? std::max(nv - 1, 0) : j;
   a.nrhs = nrhs; a.ctx = ctx; a.rb = op->rb;
+  a.wlast = last_v_stored(op, l) ? 1 : 0;
   a.ntx = (a.g.nx + 31) / 32;
   // tile height: 8 rows; the plain matvec can use 16 (HELM_MATVEC_BY=16: half the y-halo
   // overhead per point, one CTA covers 32 x 16 points)
@@ -716,17 +737,43 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
     // fused steps that form v_nv (nv > 0): split raw / formed rings (stencil.cuh FormSlot) when
     // every operand comes by TMA. Same-box A/B (profiles/r02/probe_split_ab.txt): with fewer,
     // deeper CTAs the split ring loses on steps 1-3 (the per-plane wait/form/compute chain of a
-    // CTA is the limit, not bytes in flight) and wins on the last complex128 step (NV = 4:
-    // +8 % at level 0, +7 % at level 1). HELM_SPLIT: 0 off, 1 (default) that step only, 2 all.
-    static const int split_mode = env_int("HELM_SPLIT", 1);
+    // CTA is the limit, not bytes in flight) and won on the last complex128 step (NV = 4) while
+    // that step stored V_4. Since the last step stores nothing (last_v_stored), the single ring
+    // wins there too (profiles/r02/ab_r2q: cfg4 level 0 2334 -> 2001 us, level 1 325 -> 280 us,
+    // level 2 64 -> 58 us). HELM_SPLIT: 0 (default) off, 1 the last complex128 step, 2 all.
+    static const int split_mode = env_int("HELM_SPLIT", 0);
     const bool split = a.tma && a.tmq && nv > 0 &&
                        (split_mode == 2 || (split_mode == 1 && sizeof(R) == 8 && mode == 4 && nv >= 4));
     auto go = [&](auto c) {
       constexpr int NVc = decltype(c)::value;
       if constexpr (NVc > 0) {
         if (split) {
+          if constexpr (NVc >= 4) {
+            // one row per thread (256-thread CTAs, 2 per SM): twice the warps of the 2-row
+            // split kernel for the last step's five-tile stages (HELM_SPLIT_PY=1, A/B)
+            static const bool py1 = env_int("HELM_SPLIT_PY", 2) == 1;
+            if (py1 && mode == 4) {
+              run_plane<R, 4, NVc, true, 1, true>(a, groups, units, op->st);
+              return;
+            }
+          }
           if (mode == 3) run_plane<R, 3, NVc, true, plane_py<3, true>(), true>(a, groups, units, op->st);
           else run_plane<R, 4, NVc, true, plane_py<4, true>(), true>(a, groups, units, op->st);
+          return;
+        }
+      }
+      if constexpr (NVc >= 3 && NVc <= 4) {
+        // one row per thread (256-thread CTAs, <= 128 registers, two per SM) for the steps
+        // with four or five halo'd tiles per stage, whose 2-row CTAs fit only two per SM
+        // (8 warps). HELM_FUSED_PY1 = the first step NV that uses it (default 3), MODE 3 only
+        // unless HELM_FUSED_PY1_LAST=1. Same-box A/B (profiles/r02/ab_r2s): step 3 at cfg4
+        // level 1 253 -> 243 us, level 0 1897 -> 1861 us; the last step (stores nothing,
+        // fewer operands per point) loses: 277 -> 292 us.
+        static const int py1_from = env_int("HELM_FUSED_PY1", 3);
+        static const bool py1_last = env_int("HELM_FUSED_PY1_LAST", 0) != 0;
+        if (nv >= py1_from && (mode == 3 || py1_last)) {
+          if (mode == 3) run_plane<R, 3, NVc, true, 1>(a, groups, units, op->st);
+          else run_plane<R, 4, NVc, true, 1>(a, groups, units, op->st);
           return;
         }
       }
@@ -778,14 +825,14 @@ void launch_update(helm_op* op, int l, int nrhs, const VPtrs<R>& V, int j, cx<R>
 
 template <typename R>
 void launch_solupdate(helm_op* op, int l, int nrhs, const VPtrs<R>& Z, const double* zscale, cx<R>* x,
-                      int init, int k, const KCtx& ctx) {
+                      int init, int k, const KCtx& ctx, const cx<R>* W = nullptr) {
   const long long N = op->lev[l].N;
   if (!op->nact) return;
   dim3 grid(blas_blocks(N, op->nact), op->nact);
   prof_begin(KC_SOLUPD, op->st, l);
   dispatch_k(k, [&](auto c) {
     pdl_launch(k_solupdate_t<R, decltype(c)::value>, grid, dim3(HELM_RED_THREADS), 0, op->st, N, Z, zscale, x, init,
-               (const int*)op->active_d, ctx);
+               (const int*)op->active_d, ctx, W);
   });
   CKL();
   prof_end(KC_SOLUPD, op->st, acct(op, l, (k + (init ? 1.0 : 2.0)) * sizeof(cx<R>) * N, false, nrhs));
@@ -862,7 +909,8 @@ void krylov(helm_op* op, int l, int adj, int nrhs, KCtx& ctx, int ko, int ki, bo
                         j, ctx, j == 0 ? nullptr : V[j]);
       }
       VPtrs<R> Vp = vptrs<R>(V, v0, ki);
-      launch_solupdate<R>(op, l, nrhs, Vp, ctx.scale, x, first_zero, ki, ctx);
+      launch_solupdate<R>(op, l, nrhs, Vp, ctx.scale, x, first_zero, ki, ctx,
+                          (ki >= 2 && !last_v_stored(op, l)) ? Wb[(ki - 2) & 1] : nullptr);
       continue;
     }
     for (int j = 0; j < ki; ++j) {

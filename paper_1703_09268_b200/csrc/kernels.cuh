@@ -84,6 +84,9 @@ __device__ inline void start_cycle(const KCtx& ctx, int r, double beta) {
 
 // Back substitution R y = g over the cycle's kact columns (the rotated Hessenberg), once
 // per RHS when the last column closes; the solution update then only reads y.
+// (These scalar routines run in one thread at the tail of a launch: the 3D plane kernel
+// stages the RHS's Krylov state in shared memory first, stencil.cuh KStage, so each
+// dependent access is a shared-memory access, not an L2 round trip.)
 __device__ inline void solve_ls(const KCtx& ctx, int r) {
   constexpr int K1 = HELM_KMAX + 1;
   const int k = ctx.kact[r];
@@ -102,8 +105,9 @@ __device__ inline void solve_ls(const KCtx& ctx, int r) {
 
 // Column j of the Hessenberg of RHS r is complete once h_{j+1,j} = hn is known: apply the
 // previous Givens rotations to it, form rotation j, rotate g (residual estimate |g_{j+1}|),
-// set the lazy scale of v_{j+1}, and apply the exact-breakdown guard (D14).
-__device__ inline void finalize_column(const KCtx& ctx, int r, int j, double hn) {
+// set the lazy scale of v_{j+1}, and apply the exact-breakdown guard (D14). Returns the
+// RHS's active Krylov dimension afterwards.
+__device__ inline int finalize_column(const KCtx& ctx, int r, int j, double hn) {
   constexpr int K1 = HELM_KMAX + 1;
   double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
   double* cs = ctx.cs + r * HELM_KMAX;
@@ -135,7 +139,9 @@ __device__ inline void finalize_column(const KCtx& ctx, int r, int j, double hn)
   } else {
     ctx.scale[r * K1 + j + 1] = 1.0 / hn;
   }
-  if (j + 1 >= ctx.kact[r]) solve_ls(ctx, r);        // the cycle's last column closed
+  const int kact = ctx.kact[r];
+  if (j + 1 >= kact) solve_ls(ctx, r);                // the cycle's last column closed
+  return kact;
 }
 
 // ================================================================= a1: setup (D2-D4, D6, D13)
@@ -563,23 +569,35 @@ k_update_t(long long N, VPtrs<R> V, int j, cx<R>* __restrict__ w, const int* __r
 }
 
 // x <- (init ? 0 : x) + sum_{i<kact} y_i z_i, R y = g by back substitution (per block).
+// W != null (3D unpreconditioned GMRES, whose last fused step does not store z_{K-1}): when
+// the cycle ran all K steps, z_{K-1} = fc_{K-1} W + sum_{i<K-1} fc_i z_i (the forming
+// coefficients that step saved) is folded into the coefficients and W read in its place.
 template <typename R, int K>
 __global__ void __launch_bounds__(HELM_RED_THREADS)
 k_solupdate_t(long long N, VPtrs<R> Z, const double* __restrict__ zscale, cx<R>* __restrict__ x, int init,
-              const int* __restrict__ active, KCtx ctx) {
+              const int* __restrict__ active, KCtx ctx, const cx<R>* __restrict__ W) {
   pdl_wait();
   pdl_trigger();
   const int r = active ? active[blockIdx.y] : blockIdx.y;   // compact list of active RHS
   __shared__ cx<R> yc[K];
   __shared__ int s_k;
-  if (threadIdx.x < K) {
+  if (threadIdx.x == 0) {
     const int K1 = HELM_KMAX + 1;
-    const int i = threadIdx.x;
     const int k = ctx.kact[r];
-    const double2 yv = ctx.y[r * HELM_KMAX + i];
-    const double sc = (zscale && i < k) ? zscale[r * K1 + i] : 1.0;
-    yc[i] = from_d<cx<R>>(make_double2(yv.x * sc, yv.y * sc));
-    if (i == 0) s_k = k;
+    double2 yd[K];
+    for (int i = 0; i < K; ++i) {
+      const double2 yv = ctx.y[r * HELM_KMAX + i];
+      const double sc = (zscale && i < k) ? zscale[r * K1 + i] : 1.0;
+      yd[i] = make_double2(yv.x * sc, yv.y * sc);
+    }
+    if (W && k == K && K > 1) {
+      const double2* fc = ctx.fc + r * K1;
+      const double2 yl = yd[K - 1];
+      for (int i = 0; i < K - 1; ++i) yd[i] = cadd(yd[i], cmul(yl, fc[i]));
+      yd[K - 1] = make_double2(yl.x * fc[K - 1].x, yl.y * fc[K - 1].x);
+    }
+    for (int i = 0; i < K; ++i) yc[i] = from_d<cx<R>>(yd[i]);
+    s_k = k;
   }
   __syncthreads();
   const int k = s_k;
@@ -590,6 +608,7 @@ k_solupdate_t(long long N, VPtrs<R> Z, const double* __restrict__ zscale, cx<R>*
   const cx<R>* zp[K];
 #pragma unroll
   for (int i = 0; i < K; ++i) { yl[i] = yc[i]; zp[i] = Z.p[i] + off; }
+  if (W && k == K) zp[K - 1] = W + off;
   const long long gs = (long long)gridDim.x * blockDim.x;
   long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   for (; p + gs < N; p += 2 * gs) {

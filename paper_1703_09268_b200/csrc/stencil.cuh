@@ -114,6 +114,11 @@ template <typename R> struct PlaneArgs {
   int S;                   // ring stages (>= 4; split-ring fused steps: raw stages D >= 2)
   int nf;                  // split-ring fused steps: formed slots (3: two barriers per plane, 4: one)
   int prev;                // single ring: plane z-1 from registers (S-2 planes in flight)
+  int wlast;               // MODE 4 (NV > 0): store V_NV (0: not stored — the solution update reforms
+                           // it from W and V_0..V_{NV-1} with the coefficients the epilogue saves)
+  int ctared;              // reduction tail: one slot per CTA, summed by the last CTA (0: per warp)
+  int cont;                // fused steps with TMA-only stages: one ring across the CTA's items
+                           // (the next item's planes are in flight while this one finishes)
   int tma;                 // TMA stages (tm[0] = x / W, tm[1 + i] = V_i halo'd tiles; tmm = m, tmz = z
                            // coefficients) instead of per-thread cp.async
   CUtensorMap tm[HELM_KMAX + 1];
@@ -243,6 +248,90 @@ __device__ __forceinline__ bool warp_slot_reduce(double2 (&v)[NV], double2* part
   return true;
 }
 
+// Deterministic CTA-level reduction into per-RHS slots (3D plane kernel): the CTA's warps
+// are summed in smem (fixed warp order) into ONE slot per CTA; the CTA that brings the ticket
+// to `nslots` sums all slots with every thread (strided, four independent loads in flight per
+// thread, then a fixed shuffle / warp tree). Versus one slot per warp summed by one warp
+// (warp_slot_reduce) this is 4x fewer slots and 4x the readers: the tail of a launch is one
+// or two L2 round trips instead of nslots/128 (measured: ~5 us per launch at 2,400 slots).
+// `scratch` is shared memory free for reuse (the ring, after the last item). Returns true in
+// every thread of the last CTA (false elsewhere); the totals tot[] are valid in thread 0.
+template <int NV, int NT>
+__device__ __forceinline__ bool cta_slot_reduce(double2 (&v)[NV], double2* part, unsigned* ticket, int slot, int nslots,
+                                                double2 (&tot)[NV], double2* scratch) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned* flag = reinterpret_cast<unsigned*>(scratch + NW * NV);
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v[k].x += __shfl_xor_sync(0xffffffffu, v[k].x, o);
+      v[k].y += __shfl_xor_sync(0xffffffffu, v[k].y, o);
+    }
+  __syncthreads();   // every thread is done with the ring that scratch aliases
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) scratch[warp * NV + k] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double2 t = scratch[k];
+      for (int w = 1; w < NW; ++w) { t.x += scratch[w * NV + k].x; t.y += scratch[w * NV + k].y; }
+      part[(size_t)slot * NV + k] = t;
+    }
+    __threadfence();
+    *flag = atomicAdd(ticket, 1u) == (unsigned)(nslots - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!*flag) return false;
+  __threadfence();
+  double2 t[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) t[k] = make_double2(0.0, 0.0);
+  int sl = threadIdx.x;
+  for (; sl + 3 * NT < nslots; sl += 4 * NT) {
+    double2 u[4][NV];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) u[q][k] = __ldcg(part + (size_t)(sl + q * NT) * NV + k);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) { t[k].x += u[q][k].x; t[k].y += u[q][k].y; }
+  }
+  for (; sl < nslots; sl += NT)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double2 u = __ldcg(part + (size_t)sl * NV + k);
+      t[k].x += u.x;
+      t[k].y += u.y;
+    }
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t[k].x += __shfl_xor_sync(0xffffffffu, t[k].x, o);
+      t[k].y += __shfl_xor_sync(0xffffffffu, t[k].y, o);
+    }
+  __syncthreads();   // thread 0's reads of the first scratch use are done
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) scratch[warp * NV + k] = t[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      tot[k] = scratch[k];
+      for (int w = 1; w < NW; ++w) { tot[k].x += scratch[w * NV + k].x; tot[k].y += scratch[w * NV + k].y; }
+    }
+    *ticket = 0u;
+  }
+  return true;
+}
+
 // Per-RHS epilogue of the stencil modes, run by one lane of the last-arriving warp with the
 // reduced totals: MODE 1 starts a Krylov cycle (beta = ||r||); MODE 2 stores projection
 // column jstep; MODE 3/4 finalise column NV-1 with h_{NV,NV-1} = ||V_NV|| (D14 guard), store
@@ -258,24 +347,105 @@ __device__ inline void plane_epilogue(const KCtx& ctx, int r, int jstep, const d
     double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
     for (int i = 0; i < NV; ++i) H[hidx(i, jstep)] = make_double2(tot[i].x * scl[i], tot[i].y * scl[i]);
   } else if constexpr (MODE >= 3) {
-    if constexpr (NV > 0) finalize_column(ctx, r, NV - 1, sqrt(tot[NV + 1].x));
+    if constexpr (LAST && NV > 0) {
+      // the forming coefficients of V_NV (column NV-1 is still unrotated here): the solution
+      // update reforms V_NV from W and V_0..V_{NV-1} when this step does not store it
+      const double* s = ctx.scale + r * K1;
+      const double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
+      double2* fc = ctx.fc + r * K1;
+      for (int i = 0; i < NV; ++i) {
+        const double2 h = H[hidx(i, NV - 1)];
+        fc[i] = make_double2(-h.x * s[i], -h.y * s[i]);
+      }
+      fc[NV] = make_double2(s[NV - 1], 0.0);
+    }
+    // the lazy scales s_0..s_{NV-1} are loaded before finalize_column (which only writes
+    // s_NV = 1/||V_NV||, or 0 on breakdown, i.e. when it leaves kact = NV): no dependent reload
     const double* scl = ctx.scale + r * K1;
-    const double sj = scl[NV];
+    double sv[NV + 1];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) sv[i] = scl[i];
+    int kact = HELM_KMAX;
+    if constexpr (NV > 0) {
+      const double hn = sqrt(tot[NV + 1].x);
+      kact = finalize_column(ctx, r, NV - 1, hn);
+      sv[NV] = kact == NV ? 0.0 : 1.0 / hn;
+    } else {
+      sv[0] = scl[0];
+      if constexpr (LAST) kact = ctx.kact[r];
+    }
+    const double sj = sv[NV];
     double2* H = ctx.H + (long long)r * K1 * HELM_KMAX;
     double hh = 0.0;
+#pragma unroll
     for (int i = 0; i <= NV; ++i) {
-      const double f = scl[i] * sj;
+      const double f = sv[i] * sj;
       const double2 h = make_double2(tot[i].x * f, tot[i].y * f);
       H[hidx(i, NV)] = h;
       hh += cabs2(h);
     }
     if constexpr (LAST) {
-      if (NV < ctx.kact[r]) {   // column NV is live (no breakdown above)
+      if (NV < kact) {          // column NV is live (no breakdown above)
         const double w2 = sj * sj * tot[NV + 2].x;
         finalize_column(ctx, r, NV, sqrt(fmax(w2 - hh, 0.0)));
       }
     }
   }
+}
+
+// The launch's scalar epilogue runs in ONE thread and is a chain of dependent accesses to the
+// RHS's Krylov state (Givens rotations, back substitution: ~1 us per rotation from L2,
+// measured at cfg3). KStage: warp 0 of the last CTA copies that state into shared memory
+// (independent loads, one round trip), lane 0 runs the epilogue on the copy through a KCtx
+// view (generic pointers into shared memory, RHS index 0), and the warp writes it back.
+struct KStage {
+  static constexpr int K1 = HELM_KMAX + 1;
+  // double2 units: H, sn, g, y, fc, then the reals scale, cs, beta and the int kact
+  static constexpr int oH = 0, oSn = oH + K1 * HELM_KMAX, oG = oSn + HELM_KMAX, oY = oG + K1, oFc = oY + HELM_KMAX,
+                       oReal = oFc + K1;
+  static constexpr int nReal = K1 + HELM_KMAX + 1;   // scale, cs, beta (doubles)
+  static constexpr int bytes = oReal * 16 + nReal * 8 + 16;
+  __device__ static KCtx view(unsigned char* base, int k) {
+    double2* d2 = reinterpret_cast<double2*>(base);
+    double* d1 = reinterpret_cast<double*>(d2 + oReal);
+    KCtx s{};
+    s.H = d2 + oH; s.sn = d2 + oSn; s.g = d2 + oG; s.y = d2 + oY; s.fc = d2 + oFc;
+    s.scale = d1; s.cs = d1 + K1; s.beta = d1 + K1 + HELM_KMAX;
+    s.kact = reinterpret_cast<int*>(d1 + nReal);
+    s.k = k;
+    return s;
+  }
+  template <bool IN, typename T> __device__ static void cp(T* g, T* sm, int n, int lane) {
+    for (int i = lane; i < n; i += 32) {
+      if (IN) sm[i] = g[i];
+      else g[i] = sm[i];
+    }
+  }
+  template <bool IN> __device__ static void copy(const KCtx& g, int r, const KCtx& s, int lane) {
+    cp<IN>(g.H + (long long)r * K1 * HELM_KMAX, s.H, K1 * HELM_KMAX, lane);
+    cp<IN>(g.sn + r * HELM_KMAX, s.sn, HELM_KMAX, lane);
+    cp<IN>(g.g + r * K1, s.g, K1, lane);
+    cp<IN>(g.y + r * HELM_KMAX, s.y, HELM_KMAX, lane);
+    cp<IN>(g.fc + r * K1, s.fc, K1, lane);
+    cp<IN>(g.scale + r * K1, s.scale, K1, lane);
+    cp<IN>(g.cs + r * HELM_KMAX, s.cs, HELM_KMAX, lane);
+    cp<IN>(g.beta + r, s.beta, 1, lane);
+    cp<IN>(g.kact + r, s.kact, 1, lane);
+  }
+};
+
+// plane_epilogue on the shared-memory copy of RHS r's Krylov state; called by warp 0 (all
+// lanes) of the last CTA, tot[] valid in lane 0; `sm` = KStage::bytes of free shared memory.
+template <int MODE, int NV, int NVR>
+__device__ __forceinline__ void plane_epilogue_staged(const KCtx& ctx, int r, int jstep, const double2 (&tot)[NVR],
+                                                      unsigned char* sm) {
+  const int lane = threadIdx.x & 31;
+  const KCtx s = KStage::view(sm, ctx.k);
+  KStage::copy<true>(ctx, r, s, lane);
+  __syncwarp();
+  if (lane == 0) plane_epilogue<MODE, NV>(s, 0, jstep, tot);
+  __syncwarp();
+  KStage::copy<false>(ctx, r, s, lane);
 }
 
 // DESIGN R35 (3D "compact 27-pt", P:204 [60]) at one point: L u + omega^2 M (m u) over the
@@ -311,9 +481,8 @@ __device__ __forceinline__ cx<R> opt27(const cx<R>* const (&X)[3], const R* cons
   return mkc(acc.x + wm * ms.x, acc.y + wm * ms.y);
 }
 
-template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC, bool SPLIT = false, int ST = 0>
-__global__ void __launch_bounds__(BX * BY / PY)
-k_plane(const __grid_constant__ PlaneArgs<R> a) {
+template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC, bool SPLIT, int ST>
+__device__ __forceinline__ void plane_body(const PlaneArgs<R>& a) {
   pdl_wait();
   pdl_trigger();
   using C = cx<R>;
@@ -397,6 +566,66 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
   // halos meet in L2)
   const int ntile = a.ntx * a.nty;
   const int nitems = ntile * a.nzc;
+
+  // TMA fill of stage `stg` with plane z of tile `tile`: one elected thread issues the boxes
+  // (halo'd tiles, m, the z row); every thread flips the stage's expected parity
+  auto tma_fill = [&](int tile, int z, int stg) {
+    if (threadIdx.x == 0) {
+      const int txb = tile % a.ntx, tyb = tile / a.ntx;
+      const unsigned st = sbase + (unsigned)(stg * SM::stage_bytes);
+      fence_proxy_async();   // the stage's previous contents were read / formed by the generic proxy
+      const unsigned bar = mbase + 8 * stg;
+      // full boxes (OOB zero-filled): the halo'd tiles, m's own points, the z row
+      mbar_expect_tx(bar, (unsigned)(NX * SM::XE * sizeof(C) +
+                                     (tmq ? (SM::MR ? (ST == 1 ? SM::MEm : SM::PE) * sizeof(R) : 0) + 4 * sizeof(C)
+                                          : 0)));
+      constexpr int CR = (int)(sizeof(C) / 8);   // tensor element = one 8-byte word
+#pragma unroll
+      for (int t = 0; t < NX; ++t)
+        tma_load4(st + (unsigned)(t * SM::XS * sizeof(C)), &a.tm[t], bar, CR * (txb * BX - XO), tyb * BY - YH, z,
+                  rhs[0]);
+      if (tmq) {
+        if constexpr (ST == 1) tma_load3(st + (unsigned)SM::m_off, &a.tmm, bar, txb * BX - SM::XOm, tyb * BY - 1, z);
+        else if constexpr (SM::MR) tma_load3(st + (unsigned)SM::m_off, &a.tmm, bar, txb * BX, tyb * BY, z);
+        tma_load2(st + (unsigned)SM::z_off, &a.tmz, bar, 0, zrow0 + z);
+      }
+    }
+    pbits ^= 1u << stg;
+  };
+
+  // Continuous ring (fused Arnoldi steps whose stages are filled by TMA alone): the CTA's
+  // items form ONE stream of planes (z0-1 .. z1 of each item in turn) through the ring, so
+  // the first planes of the next item are already in flight while this item's last planes
+  // are computed (no ring refill bubble per item; measured at cfg4 level 1: 9 items per CTA).
+  // The loader cursor (item, plane, stage) advances in the order the stages are freed.
+  constexpr bool CONT_OK = MODE >= 3 && !SPLIT && ST == 0;
+  const bool cont = CONT_OK && tma && tmq && a.prev != 0 && a.cont != 0;
+  // (the item's tile, first plane and plane count are derived once per item: integer division
+  // per plane in every thread cost 15 % more instructions, measured)
+  int l_it = cig, l_q = 0, l_stg = 0, c_stg = 0, l_tile = 0, l_z = 0, l_nq = 0;
+  auto loader_item = [&]() {
+    if (l_it < nitems) {
+      const int zc = l_it / ntile;
+      l_tile = l_it - zc * ntile;
+      l_z = zc * a.zlen - 1;
+      l_nq = min(nz, zc * a.zlen + a.zlen) - zc * a.zlen + 2;
+    }
+  };
+  auto loader_next = [&]() {
+    if (l_it < nitems) {
+      tma_fill(l_tile, l_z + l_q, l_stg);
+      if (++l_q == l_nq) {
+        l_q = 0;
+        l_it += a.cpg;
+        loader_item();
+      }
+    }
+    l_stg = l_stg + 1 == S ? 0 : l_stg + 1;
+  };
+  if (cont) loader_item();
+  if (cont && ract)
+    for (int q = 0; q < S; ++q) loader_next();   // the first S planes of the stream
+
   for (int it = cig; it < (ract ? nitems : 0); it += a.cpg) {
     const int tile = it % ntile, zc = it / ntile;
     const int z0 = zc * a.zlen, z1 = min(nz, z0 + a.zlen);
@@ -452,26 +681,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
         const unsigned st = sbase + (unsigned)(stg * SM::stage_bytes);
         const long long zo = (long long)z * plane;
         if (tma) {
-          if (threadIdx.x == 0) {
-            fence_proxy_async();   // the stage's previous contents were read / formed by the generic proxy
-            const unsigned bar = mbase + 8 * stg;
-            // full boxes (OOB zero-filled): the halo'd tiles, m's own points, the z row
-            mbar_expect_tx(bar, (unsigned)(NX * SM::XE * sizeof(C) +
-                                           (tmq ? (SM::MR ? (ST == 1 ? SM::MEm : SM::PE) * sizeof(R) : 0) +
-                                                      4 * sizeof(C)
-                                                : 0)));
-            constexpr int CR = (int)(sizeof(C) / 8);   // tensor element = one 8-byte word
-#pragma unroll
-            for (int t = 0; t < NX; ++t)
-              tma_load4(st + (unsigned)(t * SM::XS * sizeof(C)), &a.tm[t], bar, CR * (txb * BX - XO), tyb * BY - YH, z,
-                        rhs[0]);
-            if (tmq) {
-              if constexpr (ST == 1) tma_load3(st + (unsigned)SM::m_off, &a.tmm, bar, txb * BX - SM::XOm, tyb * BY - 1, z);
-              else if constexpr (SM::MR) tma_load3(st + (unsigned)SM::m_off, &a.tmm, bar, txb * BX, tyb * BY, z);
-              tma_load2(st + (unsigned)SM::z_off, &a.tmz, bar, 0, zrow0 + z);
-            }
-          }
-          pbits ^= 1u << stg;
+          tma_fill(tile, z, stg);
         } else {
 #pragma unroll
           for (int t = 0; t < NX; ++t) {
@@ -617,7 +827,7 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           }
           acc[NV] = cdot_acc(acc[NV], to_d(cur), hd);
           if constexpr (NV > 0) {
-            a.vout[gofs[k] + zo] = cur;
+            if (!LAST || a.wlast) a.vout[gofs[k] + zo] = cur;
             nrm += (double)cur.x * cur.x + (double)cur.y * cur.y;
           }
         }
@@ -694,21 +904,23 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
       // stage of z-1 is free, so S-2 planes are in flight (the ncu stall profile of the fused
       // steps at cfg4 level 1 showed 20 % of warp time waiting for TMA stages with S-3 = 1)
       auto inc = [S](int x) { return x + 1 == S ? 0 : x + 1; };
-      for (int q = 0; q < S; ++q) load(q, q);      // planes z0-1 .. z0+S-2
+      const int s_m1 = cont ? c_stg : 0;           // stage of plane z0-1
+      if (!cont)
+        for (int q = 0; q < S; ++q) load(q, q);    // planes z0-1 .. z0+S-2 (cont: already in flight)
+      if constexpr (!SM::MR) { ldm(z0, mr0); ldm(z0 + 1, mr1); }
       if (cpa_on) cpa_wait_n(S - 1);               // plane z0-1 (this thread's copies)
-      if (tma) mbar_wait(mbase, (pbits & 1u) ^ 1u);
+      if (tma) mbar_wait(mbase + 8 * s_m1, ((pbits >> s_m1) & 1u) ^ 1u);
       csync<YC>();
       if constexpr (FORM) {
-        form(0);
+        form(s_m1);
         csync<YC>();
       }
       {
-        const C* Xm = reinterpret_cast<const C*>(smem);
+        const C* Xm = reinterpret_cast<const C*>(smem + s_m1 * SM::stage_bytes);
 #pragma unroll
         for (int k = 0; k < PY; ++k) prevc[k] = rok[k] ? Xm[(ty0 + k * RS + YH) * XP + tx + XO] : zero;
       }
-      if constexpr (!SM::MR) { ldm(z0, mr0); ldm(z0 + 1, mr1); }
-      int s_fr = 0, s_0 = 1, s_p1 = 2;             // stages of planes z-1 (free), z, z+1
+      int s_fr = s_m1, s_0 = inc(s_m1), s_p1 = inc(s_0);   // stages of planes z-1 (free), z, z+1
       for (int z = z0; z < z1; ++z) {
         const int q = z - z0 + 1;
         if (cpa_on) cpa_wait_n(S - 3);   // this thread's groups <= q+1 complete (committed: <= q+S-2)
@@ -724,7 +936,8 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
           form(s_p1);
         }
         csync<YC>();
-        load(q + S - 1, s_fr);           // S-2 planes in flight while plane z is computed
+        if (cont) loader_next();         // the stream's next plane into the freed stage s_fr
+        else load(q + S - 1, s_fr);      // S-2 planes in flight while plane z is computed
         const unsigned char* st1 = smem + s_0 * SM::stage_bytes;
         if constexpr (!SM::MR) ldm(z + 2, mr2);
         compute(z, nullptr, reinterpret_cast<const C*>(st1), reinterpret_cast<const C*>(smem + s_p1 * SM::stage_bytes),
@@ -733,6 +946,13 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
         s_fr = s_0;
         s_0 = s_p1;
         s_p1 = inc(s_p1);
+      }
+      if (cont) {
+        // planes z1-1 and z1 (stages s_fr, s_0) are free once every thread is past compute(z1-1)
+        csync<YC>();
+        loader_next();
+        loader_next();
+        c_stg = s_p1;                    // the next item's plane z0'-1
       }
     } else {
       // ring stages are tracked incrementally (no division on the streaming path)
@@ -771,22 +991,46 @@ k_plane(const __grid_constant__ PlaneArgs<R> a) {
         s_m1 = s_0;
       }
     }
-    cpa_wait<0>();
-    csync<YC>();       // the next item's prologue reuses the ring
+    if (!cont) {
+      cpa_wait<0>();
+      csync<YC>();     // the next item's prologue reuses the ring
+    }
   }
 
   if constexpr (MODE != 0) {
     if constexpr (MODE == 1) acc[0] = make_double2(nrm, 0.0);
     if constexpr (MODE >= 3) acc[NV + 1] = make_double2(nrm, 0.0);
     if constexpr (MODE >= 3) acc[NV + 2] = make_double2(ynrm, 0.0);
-    // every warp of the CTA belongs to RHS rhs[0] -> slots (cta in group, warp)
-    constexpr int WPB = NT / 32;
+    // every thread of the CTA belongs to RHS rhs[0] -> one slot per CTA of the group
+    // (a.ctared = 0: one slot per warp, summed by one warp — the round-2 tail, A/B)
     const int r = rhs[0];
-    const int slot = cig * WPB + (threadIdx.x >> 5);
-    const int nslots = a.cpg * WPB;
     double2 tot[NVR];
-    if (warp_slot_reduce<NVR>(acc, a.rb.part + (size_t)grp * nslots * NVR, a.rb.ticket + r, slot, nslots, tot)) {
-      if ((threadIdx.x & 31) == 0) plane_epilogue<MODE, NV>(a.ctx, r, a.jstep, tot);
+    if (a.ctared) {
+      // (the KStage copy sits 4 KB into the ring, clear of the reduction scratch)
+      if (cta_slot_reduce<NVR, NT>(acc, a.rb.part + (size_t)grp * a.cpg * NVR, a.rb.ticket + r, cig, a.cpg, tot,
+                                   reinterpret_cast<double2*>(smem)) &&
+          threadIdx.x < 32)
+        plane_epilogue_staged<MODE, NV>(a.ctx, r, a.jstep, tot, smem + 4096);
+    } else {
+      constexpr int WPB = NT / 32;
+      const int slot = cig * WPB + (threadIdx.x >> 5);
+      const int nslots = a.cpg * WPB;
+      if (warp_slot_reduce<NVR>(acc, a.rb.part + (size_t)grp * nslots * NVR, a.rb.ticket + r, slot, nslots, tot)) {
+        if ((threadIdx.x & 31) == 0) plane_epilogue<MODE, NV>(a.ctx, r, a.jstep, tot);
+      }
     }
   }
+}
+
+// The plane kernel. k_plane_o2 is the same body compiled for two resident CTAs per SM
+// (register cap 65536 / (2 NT)): the split-ring last step with one row per thread
+// (HELM_SPLIT_PY=1). (An explicit minimum of one CTA in k_plane's bounds let ptxas take up to
+// 255 registers: 128 -> 198 for the fused steps, measured — so k_plane keeps the bare bound.)
+template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC, bool SPLIT = false, int ST = 0>
+__global__ void __launch_bounds__(BX * BY / PY) k_plane(const __grid_constant__ PlaneArgs<R> a) {
+  plane_body<R, BX, BY, PY, MODE, NV, YC, SPLIT, ST>(a);
+}
+template <typename R, int BX, int BY, int PY, int MODE, int NV, bool YC, bool SPLIT = false, int ST = 0>
+__global__ void __launch_bounds__(BX * BY / PY, 2) k_plane_o2(const __grid_constant__ PlaneArgs<R> a) {
+  plane_body<R, BX, BY, PY, MODE, NV, YC, SPLIT, ST>(a);
 }

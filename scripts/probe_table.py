@@ -33,7 +33,9 @@ hbm = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspat
     "hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6548.2
 kinds = [("matvec", 0, 0, 2 * Sc + Sr), ("resid", 1, 0, 3 * Sc + Sr)]
 kinds += [(f"arnoldi{j}", 3, j, (2 if j == 0 else j + 3) * Sc + Sr) for j in range(4)]
-kinds += [("arnoldi4_last", 4, 4, 6 * Sc + Sr), ("solupdate5", 10, 5, 7 * Sc)]
+# the last step stores V_4 only with HELM_LASTV=1 (3D; the solution update reforms it otherwise)
+kinds += [("arnoldi4_last", 4, 4, (6 if os.environ.get("HELM_LASTV", "0") != "0" else 5) * Sc + Sr),
+          ("solupdate5", 10, 5, 7 * Sc)]
 kinds += [(f"fgmres{j + 1}", 2, j, (3 + j) * Sc + Sr) for j in (0, 2, 4)] + [("update2", 11, 2, 5 * Sc)]
 for l in lvls:
     if l >= len(dims):

@@ -1,14 +1,20 @@
 """GPU parity of the alternative 3D stage-fill paths, each in a fresh process (the switches are
 read once per process): per-thread cp.async instead of TMA (HELM_TMA=0), TMA tiles with m and
 the z coefficients by cp.async (HELM_TMA_MZ=0), and two rows per thread for the matvec
-(HELM_PLANE_PY=2), the single-ring fused Arnoldi steps everywhere (HELM_SPLIT=0), the split
-ring for every fused step (HELM_SPLIT=2), also with three formed slots (two barriers per
+(HELM_PLANE_PY=2), the split ring for the last fused Arnoldi step (HELM_SPLIT=1; also with one
+row per thread, HELM_SPLIT_PY=1) or for every fused step (HELM_SPLIT=2), also with three formed slots (two barriers per
 plane, HELM_SPLIT_OCC=4) or two raw stages (HELM_SPLIT_D=2), and coarse V-cycles as kernel
 one grid-synchronous launch instead of a launch sequence (HELM_PERSIST=1; the level-1
 V-cycle is also compared with the numpy mirror, <= 1e-12, and must take <= 2 launches), and
 32 x 16 matvec tiles (HELM_MATVEC_BY=16), and the round-1 single ring that keeps plane z-1 in
 shared memory (HELM_PREV=0) or keeps it in registers in every mode including the matvec
-(HELM_PREV=2). Each must match the assembled oracle H (c128 <= 1e-12, c64 <= 1e-5) for
+(HELM_PREV=2), and the fused steps' per-item ring fills (HELM_CONT=0) against the default
+continuous ring across a CTA's items, also with items shorter than the ring (HELM_PLANE_NZC=9:
+3-4 planes per item; =40: one plane per item, so the ring spans several items), the last
+fused step storing V_{k-1} (HELM_LASTV=1) instead of the solution update reforming it, and
+the per-warp reduction tail (HELM_CTA_RED=0) instead of one slot per CTA, and the fused steps
+with two rows per thread everywhere (HELM_FUSED_PY1=99) or one row for the last step too
+(HELM_FUSED_PY1_LAST=1). Each must match the assembled oracle H (c128 <= 1e-12, c64 <= 1e-5) for
 helm_apply forward / adjoint on a ragged multi-tile grid, and give a certified solve."""
 import json
 import os
@@ -68,11 +74,16 @@ print(json.dumps(out))
 
 
 @pytest.mark.parametrize("env", [{"HELM_TMA": "0"}, {"HELM_TMA_MZ": "0"}, {"HELM_PLANE_PY": "2"},
-                                 {"HELM_SPLIT": "0"}, {"HELM_SPLIT": "2"}, {"HELM_SPLIT": "2", "HELM_SPLIT_OCC": "4"},
-                                 {"HELM_SPLIT": "2", "HELM_SPLIT_D": "2"}, {"HELM_PERSIST": "1"}, {"HELM_MATVEC_BY": "16"}, {"HELM_PREV": "0"}, {"HELM_PREV": "2"}],
-                         ids=["cpasync", "tma_tiles_only", "py2", "single_ring", "split_all", "split_nf3", "split_d2",
+                                 {"HELM_SPLIT": "1"}, {"HELM_SPLIT": "1", "HELM_SPLIT_PY": "1"}, {"HELM_SPLIT": "2"}, {"HELM_SPLIT": "2", "HELM_SPLIT_OCC": "4"},
+                                 {"HELM_SPLIT": "2", "HELM_SPLIT_D": "2"}, {"HELM_PERSIST": "1"}, {"HELM_MATVEC_BY": "16"}, {"HELM_PREV": "0"}, {"HELM_PREV": "2"},
+                                 {"HELM_CONT": "0"}, {"HELM_PLANE_NZC": "9"}, {"HELM_PLANE_NZC": "40"},
+                                 {"HELM_LASTV": "1"}, {"HELM_CTA_RED": "0"}, {"HELM_FUSED_PY1": "99"},
+                                 {"HELM_FUSED_PY1_LAST": "1"}],
+                         ids=["cpasync", "tma_tiles_only", "py2", "split_last_step", "split_last_step_one_row", "split_all", "split_nf3", "split_d2",
                               "persistent_vcycle", "matvec_by16", "ring_without_register_plane",
-                              "register_plane_every_mode"])
+                              "register_plane_every_mode", "per_item_ring", "cont_ring_short_items",
+                              "cont_ring_one_plane_items", "last_basis_vector_stored", "per_warp_reduction",
+                              "fused_steps_two_rows", "fused_steps_one_row_last_step_too"])
 def test_alternative_stage_paths_match_oracle(env):
     e = dict(os.environ, PYTHONPATH=ROOT + os.pathsep + os.environ.get("PYTHONPATH", ""), **env)
     r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=e, capture_output=True, text=True, timeout=600)
