@@ -254,6 +254,8 @@ def roofline_from_profile(res, hbm, peak_kind, workload_name):
         cls_all = prof[dname]
         roof["class_all_levels"] = {"achieved": round(cls_all["bytes"] / (cls_all["ms"] / 1e3) / 1e9, 1),
                                     "share_of_step": kernel_shares.get(dname)}
+    roof = roof or {}
+    roof["kernel_ms_est"] = round(total_est, 1)   # sum of the sampled kernels' estimated time in the profiled step
     return roof, kernel_shares, level_shares
 
 
@@ -274,7 +276,9 @@ def run_ours(args, rank, size, dev):
     ms = res["ms"]
     solve_roof = {"alg_bytes_per_step": step_bytes,
                   "achieved_GBps": round(step_bytes / (ms / args.steps / 1e3) / 1e9, 1),
-                  "frac": round(step_bytes / (ms / args.steps / 1e3) / 1e9 / hbm, 4)}
+                  "frac": round(step_bytes / (ms / args.steps / 1e3) / 1e9 / hbm, 4),
+                  # GPU-busy fraction: estimated kernel time of the profiled step / timed step
+                  "kernel_time_frac": round(roof.get("kernel_ms_est", 0.0) / (ms / args.steps), 4) if roof else None}
     grid, prob = res["grid"], res["prob"]
     h2d = 8 * grid.n_interior + res["d_obs_shard_bytes"] + 8 * (len(prob.src) + len(prob.rec)) + 16 * len(prob.freqs)
     d2h = 8 * (1 + grid.n_interior)
