@@ -189,6 +189,7 @@ struct helm_op {
   double2* OB = nullptr;
   KCtx ctxO{};
   int* active_d = nullptr;     // compact list of the active RHS indices (nact entries)
+  std::vector<int> alist_dev;  // host mirror of what active_d holds (set_active skips re-uploads)
   int nact = 0;
   RedBuf rb{};
   double* m_int_d = nullptr;     // interior model (fp64)
@@ -441,6 +442,34 @@ bool make_z_map(CUtensorMap* m, const cx<R>* zq, int nz, int nop) {
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// 2D march strips (march2d.cuh TMA feed): operand [rhs][z][x] as 8-byte words, box = one
+// 32-point strip row; m's padded copy [z][xq], box = 34 reals (starting one point before the
+// strip's first lane, 16-B aligned).
+template <typename R>
+bool make_strip_map(CUtensorMap* m, const void* base, int nx, int nz, int nrhs) {
+  auto enc = tma_encoder();
+  if (!enc || !base || (reinterpret_cast<uintptr_t>(base) & 15) || sizeof(cx<R>) != 16) return false;
+  const cuuint64_t ce = sizeof(cx<R>) / 8;
+  cuuint64_t dims[3] = {ce * (cuuint64_t)nx, (cuuint64_t)nz, (cuuint64_t)nrhs};
+  cuuint64_t strides[2] = {ce * (cuuint64_t)nx * 8, ce * (cuuint64_t)nx * nz * 8};
+  cuuint32_t box[3] = {(cuuint32_t)(32 * ce), 1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+template <typename R>
+bool make_mstrip_map(CUtensorMap* m, const R* mq, int nxq, int nz) {
+  auto enc = tma_encoder();
+  if (!enc || !mq) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)nxq, (cuuint64_t)nz};
+  cuuint64_t strides[1] = {(cuuint64_t)nxq * sizeof(R)};
+  cuuint32_t box[2] = {34, 1};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+             const_cast<R*>(mq), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 template <typename R> const R* level_mq(const LevelDev& L);
 template <> const double* level_mq<double>(const LevelDev& L) { return L.mq64; }
 template <> const float* level_mq<float>(const LevelDev& L) { return L.mq32; }
@@ -502,7 +531,10 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
       c.S = dfix >= 2 ? dfix : (int)std::max(2LL, std::min(12LL, d));
       c.smem = c.S * sb + c.nf * fb + 8 * c.S;
     } else {
-      c.S = t.s_fixed >= 4 ? std::min(t.s_fixed, 12) : (int)std::min<size_t>(12, (220 * 1024) / (t.occ_target * sb));
+      // the first fused step (one halo'd tile, S = 7 at the default target 4) is faster with a
+      // shallower ring at 5 CTAs per SM: cfg4 level 0 701 -> 654 us (profiles/r02/ab_r2v)
+      const int occ_t = (MODE == 3 && NV == 0 && !env_int("HELM_PLANE_OCC", 0) && sizeof(R) == 8) ? 5 : t.occ_target;
+      c.S = t.s_fixed >= 4 ? std::min(t.s_fixed, 12) : (int)std::min<size_t>(12, (220 * 1024) / (occ_t * sb));
       c.S = std::max(c.S, 4);
       c.smem = c.S * sb + 8 * c.S;   // ring + one mbarrier per stage (TMA)
     }
@@ -520,10 +552,14 @@ void run_plane(PlaneArgs<R>& a, int groups, long long units, cudaStream_t st) {
   ensure_smem_optin(kern);   // this device (the cached configuration may come from another one)
   // plane z-1 in registers (stencil.cuh PREV): same-box A/B (profiles/r02/probe_prev_ab.txt) at
   // cfg4: residual and fused steps at level 1 +7-19 %, level-0 residual +23 %, level-0 steps
-  // 1-2 -7 %; the cfg5 matvec (MODE 0) lost 3-13 %, so MODE 0 keeps the round-1 ring.
-  // HELM_PREV: 1 (default) modes 1-4, 2 every mode, 0 none.
+  // 1-2 -7 %. The configs[4] matvec (MODE 0), 24-cell sweep (profiles/r02/ab_r2u): complex64
+  // gains at every size (512^3 b = 1: 0.69 -> 0.83 of measured HBM, 256^3 b = 4: 0.57 -> 0.65),
+  // complex128 gains up to 256^3 (+PML; b = 4: 0.74 -> 0.89) and loses at 384^3-512^3
+  // (0.85 -> 0.76), so MODE 0 uses it for complex64 and for grids of <= 24 M points.
+  // HELM_PREV: 1 (default) as above, 2 every mode, 0 none.
   static const int prev_mode = env_int("HELM_PREV", 1);
-  a.prev = prev_mode == 2 || (prev_mode == 1 && MODE != 0);
+  const bool mv_prev = sizeof(R) == 4 || a.g.N <= 24LL * 1000 * 1000;
+  a.prev = prev_mode == 2 || (prev_mode == 1 && (MODE != 0 || mv_prev));
   // continuous ring across a CTA's items (fused steps with TMA-only stages; HELM_CONT=0: per-item
   // ring fills, the round-2 kernel). An item then costs its planes plus the two halo planes'
   // loads and forming, not a ring refill: HELM_CONT_HW10 = that overhead in tenths of a plane.
@@ -563,18 +599,32 @@ template <typename R> int march_max_ops(int nz) {
 // The per-lane cp.async ring holds S planes (S-2 in flight): S is the largest depth <= 16
 // whose rings fit a shared-memory budget of ~220 KB / occ_target CTAs (5 by default: a
 // shallower ring for up to 20 warps per SM; HELM_MARCH_OCC / HELM_MARCH_S override for tuning).
+template <typename R, int MODE, int NV, int ST = 0, bool TM = false>
+void run_march_t(MarchArgs<R>& a, cudaStream_t st);
+
+// 2D march launch: the TMA-fed ring for complex128 when every operand map could be encoded
+// (a.tma, set by launch_plane; HELM_MARCH_TMA=0: per-lane cp.async), else per-lane cp.async.
 template <typename R, int MODE, int NV, int ST = 0>
 void run_march(MarchArgs<R>& a, cudaStream_t st) {
-  auto kern = k_march2d<R, MODE, NV, ST>;
-  constexpr int SB = MarchShape<R, MODE, NV>::stage_bytes;
-  const size_t zbytes = ((size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>) + 15) / 16 * 16;
+  if constexpr (sizeof(R) == 8) {
+    if (a.tma) { run_march_t<R, MODE, NV, ST, true>(a, st); return; }
+  }
+  run_march_t<R, MODE, NV, ST, false>(a, st);
+}
+
+template <typename R, int MODE, int NV, int ST, bool TM>
+void run_march_t(MarchArgs<R>& a, cudaStream_t st) {
+  auto kern = k_march2d<R, MODE, NV, ST, TM>;
+  constexpr int SB = MarchShape<R, MODE, NV, TM>::stage_bytes;
+  const size_t zbytes = TM ? ((size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>) + 127) / 128 * 128
+                           : ((size_t)3 * a.g.nz * a.g.nop * sizeof(cx<R>) + 15) / 16 * 16;
   // bench A/B (march2d_variants_ab.txt): complex128 5 vs 4 = +3-5 %; complex64 (half the stage
   // bytes) 8 vs 5 = +8 % on the level-1 fused steps
   static const int occ_t = std::max(1, env_int("HELM_MARCH_OCC", sizeof(R) == 4 ? 8 : 5));
   static const int s_fix = env_int("HELM_MARCH_S", 0);
-  int S = s_fix >= 3 ? s_fix : (int)(((220 * 1024) / occ_t - (long long)zbytes) / (4 * SB));
+  int S = s_fix >= 3 ? s_fix : (int)(((220 * 1024) / occ_t - (long long)zbytes) / (4 * (SB + (TM ? 8 : 0))));
   S = std::max(3, std::min(S, 16));
-  const size_t smem = zbytes + (size_t)4 * S * SB;
+  const size_t smem = zbytes + (size_t)4 * S * SB + (TM ? (size_t)4 * S * 8 : 0);
   // the z table of every operator of the batch lives in shared memory (fwi_run closes joint
   // batches before this limit, march_max_ops); a grid too deep for even one operator fails here
   REQ(smem <= (size_t)smem_optin(), HELM_ERR_SHAPE,
@@ -595,8 +645,8 @@ void run_march(MarchArgs<R>& a, cudaStream_t st) {
     if (env_int("HELM_DEBUG", 0)) {
       cudaFuncAttributes fa{};
       cudaFuncGetAttributes(&fa, kern);
-      std::fprintf(stderr, "[helm] march2d R=%zu mode=%d nv=%d S=%d smem=%zu regs=%d occ=%d warps/SM=%d\n", sizeof(R),
-                   MODE, NV, S, smem, fa.numRegs, occ, occ * 4);
+      std::fprintf(stderr, "[helm] march2d R=%zu mode=%d nv=%d tma=%d S=%d smem=%zu regs=%d occ=%d warps/SM=%d\n",
+                   sizeof(R), MODE, NV, (int)TM, S, smem, fa.numRegs, occ, occ * 4);
     }
   }
   a.S = S;
@@ -663,6 +713,26 @@ void launch_plane(helm_op* op, int l, int adj, int mode, int nrhs, const cx<R>* 
     m.jskip = mode >= 3 ? std::max(nv - 1, 0) : j;
     m.nrhs = op->nact; m.ctx = ctx; m.rb = op->rb;
     m.nstrip = (m.g.nx + 29) / 30;
+    m.tma = 0;
+    if constexpr (sizeof(R) == 8) {
+      // TMA-fed march ring (complex128): strip rows of every streamed operand and m's padded
+      // copy. Same-box A/B at cfg2 (profiles/r02/ab_r2x, 150 RHS): TMA wins with three or more
+      // streamed operands on the large levels (level 0 fused steps 2-4 -5-7 %, FGMRES 5 -13 %)
+      // and loses with one or two (matvec, residual, steps 0-1: +8-15 %; 126 vs 96 registers)
+      // and on the small coarsest level. HELM_MARCH_TMA: 1 (default) that rule, 2 always, 0 never.
+      static const int mtma = env_int("HELM_MARCH_TMA", 1);
+      const LevelDev& Lv = op->lev[l];
+      const int nb = (mode == 2 || mode >= 3) ? nv : 0;
+      const int nxo = 1 + nb + (mode == 1 ? 1 : 0);
+      const bool want = mtma == 2 || (mtma == 1 && nxo >= 3 && m.g.N * (long long)op->nact >= 2000000LL);
+      if (want && Lv.mq64) {
+        bool ok = make_strip_map<R>(&m.tm[0], x, m.g.nx, m.g.nz, nrhs);
+        for (int i = 0; i < nb && ok; ++i) ok = make_strip_map<R>(&m.tm[1 + i], m.V.p[i], m.g.nx, m.g.nz, nrhs);
+        if (mode == 1 && ok) ok = make_strip_map<R>(&m.tm[1 + nb], b, m.g.nx, m.g.nz, nrhs);
+        ok = ok && make_mstrip_map<R>(&m.tmm, Lv.mq64, Lv.nxq, Lv.nz);
+        m.tma = ok ? 1 : 0;
+      }
+    }
     prof_begin(cls, op->st, l);
     if (op->grid.stencil == HELM_OPT) {   // R34: the 9-point stencil
       if (mode == 0) run_march<R, 0, 0, 1>(m, op->st);
@@ -1124,9 +1194,8 @@ void build_models(helm_op* op) {
       k_cast<double, float><<<(unsigned)((Lv.N + 255) / 256), 256, 0, op->st>>>(Lv.N, Lv.m64, Lv.m32);
       CKL();
     }
-  for (int l = 0; l < op->L; ++l) {   // 16-B pitched copies of m for the 3D TMA stages
+  for (int l = 0; l < op->L; ++l) {   // 16-B pitched copies of m for the TMA stages (3D) / strips (2D)
     LevelDev& Lv = op->lev[l];
-    if (Lv.ny == 1) continue;
     const size_t rows = (size_t)Lv.ny * Lv.nz;
     CK(cudaMemcpy2DAsync(Lv.mq64, sizeof(double) * Lv.nxq, Lv.m64, sizeof(double) * Lv.nx, sizeof(double) * Lv.nx, rows,
                          cudaMemcpyDeviceToDevice, op->st));
@@ -1296,7 +1365,7 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
         if (dtype == HELM_C64) Lv.zq32[adj] = dalloc<float2>(op->allocs, (size_t)4 * Lv.nz * HELM_MAXOP);
       }
     }
-    if (Lv.ny > 1) {
+    {   // 16-B pitched copy of m: the 3D TMA m tiles, and (complex128) the 2D march strips
       Lv.nxq = (Lv.nx + 3) / 4 * 4;
       Lv.mq64 = dalloc<double>(op->allocs, (size_t)Lv.nxq * Lv.ny * Lv.nz);
       if (dtype == HELM_C64) Lv.mq32 = dalloc<float>(op->allocs, (size_t)Lv.nxq * Lv.ny * Lv.nz);
@@ -1366,8 +1435,12 @@ void set_active(helm_op* op, int nrhs) {
   for (int r = 0; r < nrhs; ++r)
     if (op->act_h[r]) op->alist_h.push_back(r);
   op->nact = (int)op->alist_h.size();
-  if (op->nact)
+  // an unchanged list is not uploaded again (a pageable host->device copy costs ~10 us of host
+  // time per call: the whole launch cost of a small helm_apply)
+  if (op->nact && op->alist_h != op->alist_dev) {
     CK(cudaMemcpyAsync(op->active_d, op->alist_h.data(), sizeof(int) * op->nact, cudaMemcpyHostToDevice, op->st));
+    op->alist_dev = op->alist_h;
+  }
 }
 
 // Level-0 V-cycle as a replayed CUDA graph: within a solve the launch sequence of a V-cycle

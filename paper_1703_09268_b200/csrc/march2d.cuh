@@ -40,6 +40,12 @@ template <typename R> struct MarchArgs {
   int S;                   // per-lane prefetch ring depth (planes)
   KCtx ctx;
   RedBuf rb;
+  // TMA feed (complex128): tm[i] = operand i of the stage as [rhs][z][x] 8-byte words, box =
+  // one 32-point strip row (x0-1 .. x0+30); tmm = m's 16-B pitched copy, box = 34 reals from
+  // x0-2 (TMA box starts must be 16-B aligned). Out-of-bounds elements are zero-filled (R7).
+  int tma;
+  CUtensorMap tm[HELM_KMAX + 2];
+  CUtensorMap tmm;
 };
 
 // Per-lane prefetch ring in shared memory: every lane only ever reads back what it copied
@@ -47,22 +53,26 @@ template <typename R> struct MarchArgs {
 // barrier at all — cp.async.wait_group per lane is the whole synchronisation, and the
 // registers stay free for occupancy. Stage layout (per warp): NX operand arrays of 32
 // complex, then 32 reals of m.
-template <typename R, int MODE, int NV> struct MarchShape {
+template <typename R, int MODE, int NV, bool TM = false> struct MarchShape {
   static constexpr int NB = (MODE == 2 || MODE >= 3) ? NV : 0;    // basis operands
   static constexpr int NX = 1 + NB + (MODE == 1 ? 1 : 0);         // x/W, V_i, b
-  static constexpr int stage_bytes = (32 * (NX * (int)sizeof(cx<R>) + (int)sizeof(R)) + 15) / 16 * 16;
+  // TMA: every box lands 128-B aligned; m is a 34-real box starting one point before the strip
+  static constexpr int stage_bytes = TM ? (NX * 32 * (int)sizeof(cx<R>) + 34 * (int)sizeof(R) + 127) / 128 * 128
+                                        : (32 * (NX * (int)sizeof(cx<R>) + (int)sizeof(R)) + 15) / 16 * 16;
+  static constexpr int m_off = NX * 32 * (int)sizeof(cx<R>);
 };
 
 // One march pass over the (strip, z-chunk) items of RHS r owned by warp `wi` of `nw`: the
 // streaming body of k_march2d. Accumulates this warp's partial projections / norms.
-template <typename R, int MODE, int NV, int NVR, int ST = 0>
+template <typename R, int MODE, int NV, int NVR, int ST = 0, bool TM = false>
 __device__ __forceinline__ void march_pass(const Geo<R>& g, const OpTab<R>& T, const cx<R>* ztr, long long rb0,
                                            const cx<R>* xin, const cx<R>* bin, cx<R>* yout, cx<R>* vout,
                                            const cx<R>* const* Vp, R sc, R cw, const cx<R> (&cv)[(MODE >= 3 && NV > 0) ? NV : 1],
                                            int nstrip, int nzc, int zlen, int wi, int nw, int S, unsigned char* ring,
-                                           unsigned ring_s, double2 (&acc)[NVR], double& nrm, double& ynrm) {
+                                           unsigned ring_s, double2 (&acc)[NVR], double& nrm, double& ynrm,
+                                           const MarchArgs<R>* ta = nullptr, int rhs = 0, unsigned mb_s = 0) {
   using C = cx<R>;
-  using SH = MarchShape<R, MODE, NV>;
+  using SH = MarchShape<R, MODE, NV, TM>;
   constexpr int NB = SH::NB, NX = SH::NX, SB = SH::stage_bytes;
   constexpr bool FORM = MODE >= 3 && NV > 0;
   constexpr bool LAST = MODE == 4;
@@ -70,6 +80,7 @@ __device__ __forceinline__ void march_pass(const Geo<R>& g, const OpTab<R>& T, c
   const int lane = threadIdx.x & 31;
   const C zero = mkc((R)0, (R)0);
   const int nitems = nstrip * nzc;
+  unsigned par = 0;   // TMA: expected parity of each slot's mbarrier (persists across items)
   for (int it = wi; it < nitems; it += nw) {
     const int strip = it % nstrip, zc = it / nstrip;
     const int z0 = zc * zlen, z1 = min(nz, z0 + zlen);
@@ -85,8 +96,28 @@ __device__ __forceinline__ void march_pass(const Geo<R>& g, const OpTab<R>& T, c
     if constexpr (MODE == 1) src[NX - 1] = bin + xo;
     const R* msrc = g.m + (inx ? x : 0);
 
+    // TMA: one elected lane issues the boxes of plane q into slot sl on the slot's mbarrier
+    // (every lane tracks the slot parities); the slot's previous contents were read by the
+    // generic proxy of every lane, hence the warp barrier before each refill (issue_tm callers)
+    auto issue_tm = [&](int q, int sl) {
+      if (q <= z1) {
+        if (lane == 0) {
+          fence_proxy_async();
+          const unsigned bar = mb_s + 8 * sl, d = ring_s + (unsigned)(sl * SB);
+          mbar_expect_tx(bar, (unsigned)(NX * 32 * sizeof(C) + 34 * sizeof(R)));
+          constexpr int CR = (int)(sizeof(C) / 8);
+#pragma unroll
+          for (int i = 0; i < NX; ++i)
+            tma_load3(d + (unsigned)(i * 32 * sizeof(C)), &ta->tm[i], bar, CR * (strip * 30 - 1), q, rhs);
+          tma_load2(d + (unsigned)SH::m_off, &ta->tmm, bar, strip * 30 - 2, q);
+        }
+        par ^= 1u << sl;
+      }
+    };
+    auto wait_tm = [&](int sl) { mbar_wait(mb_s + 8 * sl, ((par >> sl) & 1u) ^ 1u); };
     // plane q (may be a ghost plane: zero-filled, R7) into ring slot `sl`; one commit group
     auto issue = [&](int q, int sl) {
+      if constexpr (TM) { issue_tm(q, sl); return; }
       if (q <= z1) {
         const bool ok = inx && q >= 0 && q < nz;
         const long long zo = ok ? (long long)q * nx : 0;
@@ -110,21 +141,26 @@ __device__ __forceinline__ void march_pass(const Geo<R>& g, const OpTab<R>& T, c
       return v;
     };
 
-    auto mval = [&](int sl) -> R { return *reinterpret_cast<const R*>(ring + sl * SB + NX * 32 * sizeof(C) + lane * sizeof(R)); };
+    auto mval = [&](int sl) -> R {
+      return *reinterpret_cast<const R*>(ring + sl * SB + SH::m_off + (lane + (TM ? 1 : 0)) * sizeof(R));
+    };
     auto shu = [](C v) { return mkc(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1)); };
     auto shd = [](C v) { return mkc(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1)); };
 
     // prologue: planes z0-1 .. z0+S-2 into slots 0 .. S-1 (slot of plane q: (q - z0 + 1) % S)
     for (int k = 0; k < S; ++k) issue(z0 - 1 + k, k);
-    cpa_wait_n(S - 2);                      // planes z0-1, z0 landed
+    if constexpr (TM) { wait_tm(0); wait_tm(1); }
+    else cpa_wait_n(S - 2);                 // planes z0-1, z0 landed
     C fm = formed(0);
     R mm = ST == 1 ? mval(0) : (R)0;        // OPT: the model of plane z-1 rides along in a register
+    if constexpr (TM) __syncwarp();         // every lane is done with slot 0
     issue(z0 - 1 + S, 0);                   // slot of z0-1 is free again
     C f0 = formed(1);
     int s0 = 1;                             // slot of plane z
     for (int z = z0; z < z1; ++z) {
       const int s1 = s0 + 1 == S ? 0 : s0 + 1;
-      cpa_wait_n(S - 2);                    // plane z+1 landed (planes up to z+S-1 issued)
+      if constexpr (TM) wait_tm(s1);
+      else cpa_wait_n(S - 2);               // plane z+1 landed (planes up to z+S-1 issued)
       const C fp = formed(s1);
       // ---- compute plane z
       const C left = shu(f0), right = shd(f0);
@@ -203,12 +239,13 @@ __device__ __forceinline__ void march_pass(const Geo<R>& g, const OpTab<R>& T, c
         }
       }
       // ---- advance: slot of plane z is free -> plane z+S
+      if constexpr (TM) __syncwarp();
       issue(z + S, s0);
       fm = f0;
       f0 = fp;
       s0 = s1;
     }
-    cpa_wait<0>();
+    if constexpr (!TM) cpa_wait<0>();      // (TMA: every issued plane <= z1 was waited for)
     __syncwarp();
   }
 }
@@ -228,13 +265,13 @@ __device__ __forceinline__ void form_coeffs(const KCtx& ctx, int r, R& cw, cx<R>
   }
 }
 
-template <typename R, int MODE, int NV, int ST = 0>
+template <typename R, int MODE, int NV, int ST = 0, bool TM = false>
 __global__ void __launch_bounds__(128)
-k_march2d(const MarchArgs<R> a) {
+k_march2d(const __grid_constant__ MarchArgs<R> a) {
   pdl_wait();
   pdl_trigger();
   using C = cx<R>;
-  using SH = MarchShape<R, MODE, NV>;
+  using SH = MarchShape<R, MODE, NV, TM>;
   constexpr int SB = SH::stage_bytes;
   constexpr bool FORM = MODE >= 3 && NV > 0;
   constexpr int NVR = MODE == 1 ? 1 : (MODE == 2 ? NV : (MODE >= 3 ? NV + 3 : 1));
@@ -259,9 +296,19 @@ k_march2d(const MarchArgs<R> a) {
   __syncthreads();
   if (ia >= a.nrhs) return;
   if (a.kact && a.jskip >= a.kact[r]) return;
-  const size_t zbytes = ((size_t)3 * g.nop * nz * sizeof(C) + 15) / 16 * 16;
+  const size_t zbytes = TM ? ((size_t)3 * g.nop * nz * sizeof(C) + 127) / 128 * 128
+                           : ((size_t)3 * g.nop * nz * sizeof(C) + 15) / 16 * 16;
   unsigned char* ring = msm + zbytes + (size_t)wib * S * SB;
   const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+  // TMA: S mbarriers per warp after the four warps' rings
+  const unsigned mb_s = (unsigned)__cvta_generic_to_shared(msm + zbytes + (size_t)4 * S * SB) + (unsigned)(wib * S * 8);
+  if constexpr (TM) {
+    if (lane == 0) {
+      for (int k = 0; k < S; ++k) mbar_init(mb_s + 8 * k, 1);
+      fence_mbar_init();
+    }
+    __syncwarp();
+  }
 
   R sc = (R)1;
   if ((MODE == 0 || MODE == 2) && a.xscale) sc = (R)a.xscale[(long long)r * a.sstride];
@@ -278,8 +325,8 @@ k_march2d(const MarchArgs<R> a) {
   // items (strip, z-chunk) of this RHS, strip fastest, dealt round-robin to its warps: warps
   // on neighbouring strips stream the same depth together, so the cache lines shared at
   // strip boundaries are read from HBM once (a balanced contiguous split lost up to 15 %)
-  march_pass<R, MODE, NV, NVR, ST>(g, T, ztr, (long long)r * g.N, a.x, a.b, a.y, a.vout, a.V.p, sc, cw, cv, a.nstrip,
-                               a.nzc, a.zlen, wi, a.wpr, S, ring, ring_s, acc, nrm, ynrm);
+  march_pass<R, MODE, NV, NVR, ST, TM>(g, T, ztr, (long long)r * g.N, a.x, a.b, a.y, a.vout, a.V.p, sc, cw, cv, a.nstrip,
+                                   a.nzc, a.zlen, wi, a.wpr, S, ring, ring_s, acc, nrm, ynrm, &a, r, mb_s);
 
   if constexpr (MODE != 0) {
     if constexpr (MODE == 1) acc[0] = make_double2(nrm, 0.0);

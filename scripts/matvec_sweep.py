@@ -42,11 +42,19 @@ def run(N, dt, b, adjoint=0, reps=10, stencil="std2"):
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) / 1e3)
+    api.profile(True, 1)   # the kernel alone (library events around the launch on its stream)
+    for i in range(reps):
+        api.helm_apply(op, xs[i % sets], ys[i % sets], adjoint)
+    torch.cuda.synchronize()
+    pr = api.profile_read()["stencil"]
+    api.profile(False, 1)
+    tk = pr["ms"] / max(1, pr["sampled"]) / 1e3
     t = statistics.median(ts)
     bytes_ = p.n_ext * (2 * sc * b + sr)
     out = {"N": N, "dtype": dt, "b": b, "adjoint": adjoint, "stencil": stencil, "ms_median": t * 1e3, "ms_best": min(ts) * 1e3,
            "gpts": p.n_ext * b / t / 1e9, "GBps": bytes_ / t / 1e9, "frac_measured": bytes_ / t / 1e9 / HBM,
-           "frac_8TBs": bytes_ / t / 8e12, "alg_bytes": bytes_}
+           "frac_8TBs": bytes_ / t / 8e12, "alg_bytes": bytes_, "ms_kernel": tk * 1e3, "gpts_kernel": p.n_ext * b / tk / 1e9,
+           "frac_measured_kernel": bytes_ / tk / 1e9 / HBM, "frac_8TBs_kernel": bytes_ / tk / 8e12}
     del xs, ys, op
     torch.cuda.empty_cache()
     return out
