@@ -59,6 +59,10 @@ struct KCtx {
                    //                 V_{k-1} = fc_{k-1} W + sum_{i<k-1} fc_i V_i (saved by the
                    //                 last fused step, which does not store V_{k-1}, 3D)
   int k;           // inner dimension of this process
+  double* tol;     // [nrhs] or null: absolute residual-estimate tolerance for stopping INSIDE a
+                   //                 cycle (R23: the Arnoldi estimate |g_{j+1}| may end a cycle
+                   //                 early; convergence itself is decided on the true residual).
+                   //                 Only the outer FGMRES sets it.
 };
 
 __device__ __forceinline__ int hidx(int i, int j) { return i * HELM_KMAX + j; }

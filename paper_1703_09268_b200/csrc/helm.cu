@@ -202,14 +202,30 @@ struct helm_op {
   std::vector<int64_t> mv[4];
   double ws_vectors = 0.0;
   bool apply_only = false;
-  // captured level-0 V-cycles (CUDA graphs), keyed by (adjoint, batch size, active count)
-  struct VGraph { int adj, nrhs, nact; cudaGraphExec_t exec; double bytes; long long mv[4]; long long launches; };
+  // captured level-0 V-cycles (CUDA graphs), keyed by (adjoint, batch size, active count) and
+  // the operator signature `gsig` = the batch's omegas: the only values a captured kernel
+  // carries BY VALUE besides the key (omega^2 per operator and the operator count); model,
+  // tables, Krylov scalars, operator indices and the active list are device memory behind
+  // fixed pointers, rewritten in place by op_set_model / build_tables. So graphs stay valid
+  // across fwi_* calls and model updates and are only matched by signature.
+  struct VGraph {
+    int adj, nrhs, nact; cudaGraphExec_t exec; double bytes; long long mv[4]; long long launches;
+    std::vector<double> sig;
+  };
   std::vector<VGraph> vgraphs;
+  std::vector<double> gsig;
   cudaStream_t cap_st = nullptr;   // private stream for graph capture (the caller's may be legacy)
   bool graphs_off = false;         // a capture failed: run V-cycles live from then on
   void clear_graphs() {
     for (auto& g : vgraphs) cudaGraphExecDestroy(g.exec);
     vgraphs.clear();
+  }
+  void trim_graphs() {             // bounded cache: drop the oldest half
+    constexpr size_t cap = 256;
+    if (vgraphs.size() < cap) return;
+    const size_t drop = vgraphs.size() / 2;
+    for (size_t i = 0; i < drop; ++i) cudaGraphExecDestroy(vgraphs[i].exec);
+    vgraphs.erase(vgraphs.begin(), vgraphs.begin() + drop);
   }
   ~helm_op() {
     clear_graphs();
@@ -1263,7 +1279,7 @@ void validate_model_pml(const helm_grid& g, const double* m, const helm_pml& P) 
 }
 
 void op_set_model(helm_op* op, const double* m_host) {
-  op->clear_graphs();
+  // captured graphs stay valid: the models are rewritten in place (helm_op::VGraph)
   const helm_grid& G = op->grid;
   const size_t n_int = (size_t)G.n[0] * G.n[1] * G.n[2];
   CK(cudaMemcpyAsync(op->m_int_d, m_host, n_int * sizeof(double), cudaMemcpyHostToDevice, op->st));
@@ -1273,7 +1289,7 @@ void op_set_model(helm_op* op, const double* m_host) {
 void op_set_omegas(helm_op* op, const double* w, int n) {
   REQ(n >= 1 && n <= HELM_MAXOP, HELM_ERR_ARG, "too many operators in one batch");
   for (int o = 0; o < n; ++o) REQ(w[o] > 0 && std::isfinite(w[o]), HELM_ERR_ARG, "omega must be > 0");
-  op->clear_graphs();   // the captured kernels carry omega^2 and the operator count by value
+  op->gsig.assign(w, w + n);   // captured kernels carry omega^2 and the operator count by value
   op->nop = n;
   for (int o = 0; o < n; ++o) op->omegas[o] = w[o];
   op->omega = w[0];
@@ -1403,6 +1419,8 @@ helm_op* op_create(const helm_grid* grid, const double* m, double omega, const h
   for (int i = 0; i <= k_inner; ++i) op->OV[i] = dalloc<double2>(op->allocs, n0);
   for (int i = 0; i < k_inner; ++i) op->OZ[i] = dalloc<double2>(op->allocs, n0);
   op->ctxO = make_ctx(op->allocs, max_rhs, k_inner);
+  op->ctxO.tol = dalloc<double>(op->allocs, max_rhs);   // early stop inside an outer cycle (R23)
+  CK(cudaMemset(op->ctxO.tol, 0, sizeof(double) * max_rhs));
   op->ws_vectors = 2 * k_inner + 1;
   if (dtype == HELM_C64) {
     op->OX = dalloc<double2>(op->allocs, n0);
@@ -1454,7 +1472,7 @@ void vcycle0_graph(helm_op* op, int adj, int nrhs, const cx<R>* b, cx<R>* z) {
   static const bool on = env_int("HELM_GRAPHS", 1) != 0;
   if (!on || g_prof.on || op->graphs_off || op->nact == 0) { vcycle<R>(op, 0, adj, nrhs, b, z); return; }
   for (auto& g : op->vgraphs)
-    if (g.adj == adj && g.nrhs == nrhs && g.nact == op->nact) {
+    if (g.adj == adj && g.nrhs == nrhs && g.nact == op->nact && g.sig == op->gsig) {
       CK(cudaGraphLaunch(g.exec, op->st));
       for (int r = 0; r < nrhs; ++r)
         if (op->act_h[r]) {
@@ -1514,6 +1532,8 @@ void vcycle0_graph(helm_op* op, int adj, int nrhs, const cx<R>* b, cx<R>* z) {
   const cudaError_t e = cudaGraphInstantiate(&vg.exec, graph, 0);
   cudaGraphDestroy(graph);
   CK(e);
+  vg.sig = op->gsig;
+  op->trim_graphs();
   op->vgraphs.push_back(vg);
 }
 
@@ -1526,13 +1546,27 @@ void solve_c128(helm_op* op, int adj, int nrhs, const double2* B, double2* X, co
   reset_acct(op, nrhs);
   set_active(op, nrhs);
   CK(cudaMemsetAsync(X, 0, sizeof(double2) * N * nrhs, op->st));
-  KCtx& ctx = op->ctxO;
+  // Early stop inside a cycle (R23: "the Arnoldi estimate is allowed only for early stopping
+  // inside a cycle"): when the residual estimate |g_{j+1}| of a RHS reaches 0.98 rtol ||b||
+  // after inner step j, its cycle closes at j + 1 columns (finalize_column, as on a breakdown),
+  // the RHS leaves the cycle's remaining steps, and the solution update reads j + 1 columns.
+  // Convergence is still decided on the TRUE residual at the next cycle start. HELM_EARLY=0:
+  // every cycle runs all k_inner steps.
+  static const bool early = env_int("HELM_EARLY", 1) != 0;
+  KCtx ctx = op->ctxO;
   ctx.k = op->k_inner;
-  std::vector<double> bn(nrhs), beta(nrhs), rel(nrhs, 1.0);
-  std::vector<int> cycles(nrhs, 0);
+  if (!early) ctx.tol = nullptr;
+  std::vector<double> bn(nrhs), beta(nrhs), rel(nrhs, 1.0), tolh(nrhs, 0.0);
+  std::vector<int> cycles(nrhs, 0), kact_h(nrhs, 0);
   launch_norm_start<double>(op, 0, nrhs, B, ctx);
   CK(cudaMemcpyAsync(bn.data(), ctx.beta, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, op->st));
   CK(cudaStreamSynchronize(op->st));
+  if (early) {
+    // HELM_EARLY_PCT: the factor in percent (tuning / A-B; default 98)
+    static const double fac = 0.01 * std::min(100, std::max(1, env_int("HELM_EARLY_PCT", 98)));
+    for (int r = 0; r < nrhs; ++r) tolh[r] = fac * so.rtol * bn[r];
+    CK(cudaMemcpyAsync(ctx.tol, tolh.data(), sizeof(double) * nrhs, cudaMemcpyHostToDevice, op->st));
+  }
   const bool precond = so.precond != 0 && op->L >= 2;
   Precond<double> M;
   if (precond) {
@@ -1571,6 +1605,8 @@ void solve_c128(helm_op* op, int adj, int nrhs, const double2* B, double2* X, co
     if (!nact) break;
     set_active(op, nrhs);
     const int ki = op->k_inner;
+    const std::vector<int> cyc_act = op->act_h;   // the cycle's RHS (the solution update runs over these)
+    bool shrunk = false;
     for (int j = 0; j < ki; ++j) {
       VPtrs<double> Vp = vptrs<double>(op->OV, v0, j + 1);
       const double2* zj;
@@ -1585,6 +1621,25 @@ void solve_c128(helm_op* op, int adj, int nrhs, const double2* B, double2* X, co
       }
       launch_plane<double>(op, 0, adj, 2, nrhs, zj, op->OV[j + 1], nullptr, &Vp, j + 1, zs, ctx.kact, j, ctx);
       launch_update<double>(op, 0, nrhs, Vp, j, op->OV[j + 1], ctx);
+      if (early && j + 1 < ki) {
+        // RHS whose cycle closed at column j (estimate reached, or breakdown) sit out the rest
+        CK(cudaMemcpyAsync(kact_h.data(), ctx.kact, sizeof(int) * nrhs, cudaMemcpyDeviceToHost, op->st));
+        CK(cudaStreamSynchronize(op->st));
+        int still = 0;
+        bool changed = false;
+        for (int r = 0; r < nrhs; ++r) {
+          if (!op->act_h[r]) continue;
+          if (kact_h[r] <= j + 1) { op->act_h[r] = 0; changed = true; }
+          else ++still;
+        }
+        shrunk = shrunk || changed;
+        if (!still) break;
+        if (changed) set_active(op, nrhs);
+      }
+    }
+    if (shrunk) {
+      op->act_h = cyc_act;
+      set_active(op, nrhs);
     }
     if (precond) {
       VPtrs<double> Zp{};

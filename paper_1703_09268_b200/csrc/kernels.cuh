@@ -139,6 +139,13 @@ __device__ inline int finalize_column(const KCtx& ctx, int r, int j, double hn) 
   } else {
     ctx.scale[r * K1 + j + 1] = 1.0 / hn;
   }
+  // early stop inside a cycle (R23): the residual estimate |g_{j+1}| of this RHS reached its
+  // tolerance, so the cycle closes at j + 1 columns exactly like a breakdown (the host drops
+  // the RHS from the cycle's remaining steps and the solution update reads j + 1 columns).
+  if (ctx.tol && j + 1 < ctx.kact[r] && sqrt(cabs2(gv[j + 1])) <= ctx.tol[r]) {
+    ctx.kact[r] = j + 1;
+    ctx.scale[r * K1 + j + 1] = 0.0;
+  }
   const int kact = ctx.kact[r];
   if (j + 1 >= kact) solve_ls(ctx, r);                // the cycle's last column closed
   return kact;
