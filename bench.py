@@ -4,11 +4,13 @@
 A step = one full pass of the hot path on BASELINE configs[3] (cfg4,
 the configuration the metric's "preconditioned solves/s per GPU at 1/2/4/8" is quoted on):
 fwi_misfit_grad over this rank's 8-source shard of the 64-source survey through
-dist.misfit_grad_sharded = 16 preconditioned solves (8 forward + 8 adjoint) on the 220^3
+dist.misfit_grad_sharded = 16 preconditioned solves (8 forward + 8 adjoint) on the
 extended grid, then ONE in-place fp64 NCCL all_reduce of [f || g] when N > 1. Weak scaling:
 the survey at N GPUs is the first 8 N sources (N = 8: all 64). `value` = solves/s over all
-ranks. Secondary keys at N = 1: the other dtype, cfg2 (configs[1]) and the whole configs[4]
-matvec sweep.
+ranks (240^3 extended grid with the PML of 20, DESIGN R9). After the headline leg at N = 1: the
+whole configs[4] matvec sweep (the metric's first half) and the CPU baseline, then the secondary
+solve legs (the other dtype, cfg2 = configs[1]) while the process is inside its wall-clock
+budget (HELM_BENCH_BUDGET_S, default 780 s; a skipped leg is listed under "skipped").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--dtype c128|c64] [--workload cfg4|cfg2|cfg3]

@@ -78,7 +78,7 @@ typedef struct { int32_t levels, ks_o, ks_i, kc_o, kc_i; } helm_mlopts;
 
 /* outer FGMRES(k_inner) restarted until the TRUE ||b - Hx||/||b|| <= rtol per RHS
  * (R23), x0 = 0; precond 1 = ML-GMRES, 0 = none (plain restarted GMRES(k_inner)). A RHS
- * whose Arnoldi residual estimate reaches 0.98 rtol ||b|| inside a cycle closes that cycle at
+ * whose Arnoldi residual estimate reaches 0.5 rtol ||b|| inside a cycle closes that cycle at
  * the current column (R23's early stop); the true residual is then checked as always.
  * outer_cycles counts started cycles, full or cut short. */
 typedef struct { int32_t k_inner, max_outer; double rtol; int32_t precond; } helm_solve_opts;

@@ -1547,7 +1547,7 @@ void solve_c128(helm_op* op, int adj, int nrhs, const double2* B, double2* X, co
   set_active(op, nrhs);
   CK(cudaMemsetAsync(X, 0, sizeof(double2) * N * nrhs, op->st));
   // Early stop inside a cycle (R23: "the Arnoldi estimate is allowed only for early stopping
-  // inside a cycle"): when the residual estimate |g_{j+1}| of a RHS reaches 0.98 rtol ||b||
+  // inside a cycle"): when the residual estimate |g_{j+1}| of a RHS reaches 0.5 rtol ||b||
   // after inner step j, its cycle closes at j + 1 columns (finalize_column, as on a breakdown),
   // the RHS leaves the cycle's remaining steps, and the solution update reads j + 1 columns.
   // Convergence is still decided on the TRUE residual at the next cycle start. HELM_EARLY=0:
@@ -1562,8 +1562,10 @@ void solve_c128(helm_op* op, int adj, int nrhs, const double2* B, double2* X, co
   CK(cudaMemcpyAsync(bn.data(), ctx.beta, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, op->st));
   CK(cudaStreamSynchronize(op->st));
   if (early) {
-    // HELM_EARLY_PCT: the factor in percent (tuning / A-B; default 98)
-    static const double fac = 0.01 * std::min(100, std::max(1, env_int("HELM_EARLY_PCT", 98)));
+    // HELM_EARLY_PCT: the factor in percent (default 50; measured in profiles/r02/ab_r2z,
+    // gpu_tests_r2aa: at 98 exit residuals sit at 0.9-1.0 rtol and the north star's 1e-5 bar on
+    // f fails on tiny2d (1.6e-5); at 50 every parity test holds its bar)
+    static const double fac = 0.01 * std::min(100, std::max(1, env_int("HELM_EARLY_PCT", 50)));
     for (int r = 0; r < nrhs; ++r) tolh[r] = fac * so.rtol * bn[r];
     CK(cudaMemcpyAsync(ctx.tol, tolh.data(), sizeof(double) * nrhs, cudaMemcpyHostToDevice, op->st));
   }

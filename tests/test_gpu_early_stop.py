@@ -5,8 +5,8 @@ Each variant runs in a fresh process (HELM_EARLY is read once per process). Batc
 different difficulty (point sources, a smooth random RHS, a scaled copy and a zero RHS) so that
 they leave their cycles at different inner steps, forward and adjoint, 2D and 3D, c128 and c64.
 Checked against the oracle's assembled H and its LU (unique solution): certified true residual,
-point-source solutions <= 1e-5 from LU (random RHS <= 5e-5: only ||H^-1|| bounds their error
-at a residual of 1e-6), never more level-0 matvecs or cycles than full cycles take, and the
+point-source solutions <= 2e-5 from LU (random RHS <= 5e-5: only ||H^-1|| bounds the error
+at a residual of 1e-6, in either schedule), never more level-0 matvecs or cycles than full cycles take, and the
 full-cycle schedule (HELM_EARLY=0) still certifies."""
 import json
 import os
@@ -80,9 +80,13 @@ def test_early_stop_solutions_are_certified(runs):
             tol_res = 1e-6 * (1 + 1e-3) if "c128" in key else 2e-6
             assert v["conv"] and v["zero"], (key, v)
             assert v["res"] <= tol_res, (key, v)
-            # point sources (the path's workload): the north star's 1e-5; the random RHS excite
-            # every mode, their error is bounded through ||H^-1|| only (measured <= 20 x residual)
-            assert max(v["err"][:2]) <= 1e-5, (key, v)
+            # A certified residual of rtol = 1e-6 bounds the error only through ||H^-1||: on this
+            # grid the measured error / residual ratio is 4-11 for the point sources and up to 17
+            # for the random full-spectrum RHS, in BOTH schedules (full cycles, adjoint point
+            # source 1: residual 9.7e-7, error 1.05e-5), so the bars here are 2e-5 and 5e-5; the
+            # north star's 1e-5 on f, g and the BASELINE configs is checked where it is stated
+            # (test_gpu_fwi, test_gpu_solve, test_gpu_fullsize).
+            assert max(v["err"][:2]) <= 2e-5, (key, v)
             assert max(v["err"][2:]) <= 5e-5, (key, v)
 
 
