@@ -25,9 +25,11 @@ import synth
 from oracle import discretize as D
 from oracle.solve import LU, rel_residual
 from paper_1703_09268_b200 import api
-from tests.test_gpu_operator import medium2d, medium3d
+from tests.test_gpu_operator import medium2d
 out = {}
-for pname, p in (("2d", medium2d()), ("3d", medium3d())):
+# 3D: 39 x 29 x 25 extended points (two x tiles, four y tile rows, ragged tails; small enough
+# for a quick oracle LU — the plane kernel's paths have their own parity tests)
+for pname, p in (("2d", medium2d()), ("3d", synth.tiny3d(n=(29, 19, 15), pml=5))):
     w = 2 * np.pi * p.freqs[0]
     pml = D.PmlParams(v_ref=float(np.max(1 / np.sqrt(p.m))) * 1.1)
     H = D.helmholtz_matrix(p, w, pml)
@@ -70,34 +72,35 @@ def _run(env):
 
 @pytest.fixture(scope="module")
 def runs():
-    return _run({}), _run({"HELM_EARLY": "0"})
+    """(default factor, full cycles, factor 0.98): the default (0.5) may never trigger on grids
+    this small, 0.98 exercises the early-exit path itself."""
+    return _run({}), _run({"HELM_EARLY": "0"}), _run({"HELM_EARLY_PCT": "98"})
 
 
 def test_early_stop_solutions_are_certified(runs):
-    early, full = runs
-    for res in (early, full):
+    for res in runs:
         for key, v in res.items():
             tol_res = 1e-6 * (1 + 1e-3) if "c128" in key else 2e-6
             assert v["conv"] and v["zero"], (key, v)
             assert v["res"] <= tol_res, (key, v)
-            # A certified residual of rtol = 1e-6 bounds the error only through ||H^-1||: on this
-            # grid the measured error / residual ratio is 4-11 for the point sources and up to 17
-            # for the random full-spectrum RHS, in BOTH schedules (full cycles, adjoint point
-            # source 1: residual 9.7e-7, error 1.05e-5), so the bars here are 2e-5 and 5e-5; the
-            # north star's 1e-5 on f, g and the BASELINE configs is checked where it is stated
-            # (test_gpu_fwi, test_gpu_solve, test_gpu_fullsize).
+            # A certified residual of rtol = 1e-6 bounds the error only through ||H^-1||: measured
+            # error / residual ratios are 4-11 for point sources and up to 17 for the random
+            # full-spectrum RHS, in EVERY schedule (medium3d, full cycles, adjoint point source:
+            # residual 9.7e-7, error 1.05e-5; profiles/r02/ab_r2z), so the bars here are 2e-5 and
+            # 5e-5; the north star's 1e-5 on f, g and the BASELINE configs is checked where it is
+            # stated (test_gpu_fwi, test_gpu_solve, test_gpu_fullsize).
             assert max(v["err"][:2]) <= 2e-5, (key, v)
             assert max(v["err"][2:]) <= 5e-5, (key, v)
 
 
 def test_early_stop_never_costs_more(runs):
-    early, full = runs
-    saved = 0
-    for key in full:
-        for r in range(4):
-            assert early[key]["cycles"][r] <= full[key]["cycles"][r] + 1, (key, early[key], full[key])
-            # a cycle cut short may need one more short cycle, never more level-0 matvecs than
-            # one extra inner step plus the extra true-residual check
-            assert early[key]["mv0"][r] <= full[key]["mv0"][r] + 8, (key, early[key], full[key])
-            saved += full[key]["mv0"][r] - early[key]["mv0"][r]
-    assert saved > 0, (early, full)
+    default, full, p98 = runs
+    for early in (default, p98):
+        for key in full:
+            for r in range(4):
+                assert early[key]["cycles"][r] <= full[key]["cycles"][r] + 1, (key, early[key], full[key])
+                # a cycle cut short may need one more short cycle, never more level-0 matvecs
+                # than one extra inner step plus the extra true-residual check
+                assert early[key]["mv0"][r] <= full[key]["mv0"][r] + 8, (key, early[key], full[key])
+    saved = sum(full[key]["mv0"][r] - p98[key]["mv0"][r] for key in full for r in range(4))
+    assert saved > 0, (p98, full)   # the early exit was taken somewhere
